@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py -- DTR eviction-decision throughput on B200 (arXiv 2006.09616, simrd V2).
+
+Workload (BASELINE.json configs[1], "config2"): the ResNet-32-shaped synthetic op
+log, budget ratios 0.1..1.0 (30 permilles) x {h_DTR, h_DTR_eq, LRU, size} = 120
+independent simulations per GPU (weak scaling: rank r replays its own log drawn
+with seed r).  One step = one dtr_replay_batch over those 120 cells (plan kernel +
+one CTA-per-simulation engine launch) [+ one NCCL all_gather of the result rows
+when N > 1].
+
+  value   = eviction decisions / s over all ranks, device-timed (CUDA events on the
+            launching stream, max over ranks), inputs resident in HBM, L2 flushed
+            (256 MiB write) before every timed step.
+  e2e     = same metric through dtr_replay_batch_host: pinned host log + cells in,
+            rows out, H2D/D2H and stream-ordered allocation inside the timed region.
+  roofline: the CTA engine (dominant kernel): algorithmic score-pass bytes per
+            launch (sum of rows' score_bytes) / its average
+            CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
+  roofline_large_pool: the grid engine on the config-5s stress log (1e6-tensor
+            random locality DAG, pool ~1e6): per-decision bytes / per-decision time,
+            isolated as the difference of two decision caps.
+  cpu_baseline: the CPU oracle (oracle/, plain C, unmodified) on the host cores,
+            process pool, bounded sample of the same cells (rank 0, N = 1 only).
+
+`--impl reference` times the oracle alone (the reference arm for this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from dtr_inputs import LogView, models  # noqa: E402
+
+METRIC = "eviction decisions/sec (pool score+argmin) and sweep runs/sec at 1/2/4/8 B200"
+HEURS = ("dtr", "dtr_eq", "lru", "size")
+HEUR_IDS = {"dtr": 0, "dtr_eq": 1, "lru": 2, "size": 3, "msps": 4, "local": 5, "random": 6}
+
+
+def workload(rank: int):
+    """config 2: ResNet-32-shaped log (seed = rank) x 30 permilles x 4 heuristics."""
+    w = models.resnet32(seed=rank)
+    v = LogView(w)
+    specs = []
+    for h in HEURS:
+        for pm in models.sweep_permilles(30):
+            specs.append(dict(log=0, budget=v.budget(pm), heuristic=HEUR_IDS[h], thrash_kill=16,
+                              cell_id=len(specs)))
+    return [w], specs
+
+
+# ---------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,utilization.gpu,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 10]
+        load = [r for r in rows if _num(r[3]) and _num(r[3]) > 0] or rows
+        sm = [_num(r[1]) for r in load if _num(r[1])]
+        mx = [_num(r[2]) for r in rows if _num(r[2])]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in load:
+            for k, nm in enumerate(names):
+                if r[6 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(load)}
+
+
+def _num(x):
+    try:
+        return float(x)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------- cpu oracle
+
+def _oracle_cell(args):
+    words, h, budget, kill = args
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    r, _ = O.replay(words, h, budget, thrash_kill=kill)
+    return int(r["decisions"]), time.perf_counter() - t0
+
+
+def oracle_sample(logs, specs, budget_s: float, cores: int):
+    """Replay cells on `cores` processes until `budget_s` of wall time or all done."""
+    import multiprocessing as mp
+    from oracle import oracle as O
+    O.build()
+    jobs = [(logs[s["log"]], s["heuristic"], s["budget"], s.get("thrash_kill", 16)) for s in specs]
+    ctx = mp.get_context("fork")
+    done_dec, done_cells = 0, 0
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        it = pool.imap_unordered(_oracle_cell, jobs, chunksize=1)
+        for dec, _ in it:
+            done_dec += dec
+            done_cells += 1
+            if time.perf_counter() - t0 > budget_s:
+                pool.terminate()
+                break
+    wall = time.perf_counter() - t0
+    return done_dec, done_cells, wall
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------- main
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    logs, specs = workload(0)
+    cores = host_cores()
+    # each step: the whole config-2 sweep on the host cores (a bounded sample)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        dec, cells, wall = oracle_sample(logs, specs, budget_s=60.0, cores=cores)
+        if i >= args.warmup:
+            vals.append((dec, cells, wall))
+    dec = sum(v[0] for v in vals)
+    wall = sum(v[2] for v in vals)
+    cells = sum(v[1] for v in vals)
+    value = dec / wall
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "decisions/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "runs_per_sec": cells / wall,
+            "config": {"workload": "config2: resnet32-shaped log x 30 budget ratios x {h_DTR,h_DTR_eq,LRU,size}",
+                       "cells_per_step": len(specs)},
+            "cpu_baseline": {"value": value, "unit": "decisions/s", "cores": cores, "kind": "oracle",
+                             "sample": f"the full 120-cell config-2 sweep per step, {cores}-process pool"},
+            "e2e": {"value": value, "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-large-pool", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--large-n", type=int, default=1000000)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2006_09616_b200 as P
+
+    logs, specs = workload(rank)
+    batch = P.DeviceBatch(logs, specs, engine=P.ENGINE_CTA)
+    stream = torch.cuda.current_stream(dev)
+    n_cells = len(specs)
+    rows_all = torch.empty(ws * batch.rows.numel(), dtype=torch.uint8, device=dev) if ws > 1 else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        batch.run(stream)
+        if ws > 1:
+            dist.all_gather_into_tensor(rows_all, batch.rows)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    rows = batch.result_rows()
+    decisions_rank = int(rows["decisions"].sum())
+    score_bytes = int(rows["score_bytes"].sum())
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    wall = time.perf_counter() - w0
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_rank = sum(step_ms) / 1e3
+    if ws > 1:
+        t = torch.tensor([t_rank], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+        d = torch.tensor([decisions_rank], dtype=torch.int64, device=dev)
+        dist.all_reduce(d)
+        decisions_all = int(d.item())
+    else:
+        t_max = t_rank
+        decisions_all = decisions_rank
+    value = decisions_all * args.steps / t_max
+    runs_per_sec = ws * n_cells * args.steps / t_max
+
+    # ---- e2e: through the public host-buffer entry (pinned host memory)
+    words, offs = P.pack_logs(logs)
+    cells, _ = P.make_cells(offs, specs)
+    h_words = torch.from_numpy(words.view(np.int32)).pin_memory()
+    h_cells = torch.from_numpy(cells.view(np.uint8)).pin_memory()
+    h_rows = torch.empty(n_cells * P.RESULT_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+    import ctypes as C
+
+    def e2e_step():
+        rc = P.lib.dtr_replay_batch_host(C.c_void_p(h_words.data_ptr()), len(words), C.c_void_p(h_cells.data_ptr()),
+                                         n_cells, P.ENGINE_CTA, C.c_void_p(h_rows.data_ptr()), None, 0,
+                                         C.c_void_p(stream.cuda_stream))
+        assert rc == 0, rc
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    e_ms = []
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_step()
+        e_ms.append(time.perf_counter() - t0)
+    e_rank = sum(e_ms)
+    if ws > 1:
+        t = torch.tensor([e_rank], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_rank = float(t.item())
+    e2e_rows = h_rows.numpy().view(P.RESULT_DTYPE)
+    assert int(e2e_rows["decisions"].sum()) == decisions_rank
+    e2e_value = decisions_all * args.steps / e_rank
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm_peak, peak_src = float(peaks["hbm_gbs"]), "measured"
+    except Exception:
+        hbm_peak, peak_src = 6650.0, "fallback"
+    kern_s = t_rank / args.steps
+    roof = {"bound": "hbm", "achieved": score_bytes / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": score_bytes / kern_s / 1e9 / hbm_peak, "traffic": None, "peak_source": peak_src,
+            "kernel": "cta_engine", "algorithmic_bytes_per_launch": score_bytes,
+            "note": "small pools: state is L1/L2-resident, the engine is latency-bound (DESIGN.md)"}
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        try:
+            tf = json.load(open(traffic_file))
+            roof["traffic"] = tf.get("cta_engine_config2")
+        except Exception:
+            pass
+
+    out = {"metric": METRIC, "value": value, "unit": "decisions/s", "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+           "config": {"workload": "config2: resnet32-shaped log x 30 budget ratios x {h_DTR,h_DTR_eq,LRU,size}",
+                      "cells_per_gpu": n_cells, "decisions_per_gpu_step": decisions_rank,
+                      "engine": "cta (one CTA per simulation)", "l2": "flushed (256 MiB write) before each step",
+                      "parallelism": f"sweep sharded, {ws} rank(s), all_gather of rows"},
+           "runs_per_sec": runs_per_sec,
+           "e2e": {"value": e2e_value, "unit": "decisions/s",
+                   "h2d_bytes_per_step": int(words.nbytes + cells.nbytes + 12 * n_cells),
+                   "d2h_bytes_per_step": int(n_cells * P.RESULT_DTYPE.itemsize)},
+           "gpu_launches": 2 * args.steps,
+           "roofline": roof,
+           "clocks": clocks,
+           "wall_s_timed": wall}
+
+    if rank == 0 and not args.no_large_pool:
+        out["roofline_large_pool"] = large_pool(P, torch, dev, args.large_n, hbm_peak, peak_src)
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cores = host_cores()
+        dec, ncell, wsec = oracle_sample(logs, specs, budget_s=20.0, cores=cores)
+        out["cpu_baseline"] = {"value": dec / wsec, "unit": "decisions/s", "cores": cores, "kind": "oracle",
+                               "sample": f"{ncell} of the {n_cells} config-2 cells, {cores}-process pool, "
+                                         f"{wsec:.2f} s"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def large_pool(P, torch, dev, n, hbm_peak, peak_src):
+    """Grid engine on the config-5s stress log: per-decision score+argmin cost at a ~n pool."""
+    w = models.random_dag(n, seed=0)
+    v = LogView(w)
+    res = {}
+    for D in (32, 160):
+        spec = [dict(log=0, budget=v.peak_total * 98 // 100, heuristic=0, thrash_kill=16, max_decisions=D)]
+        b = P.DeviceBatch([w], spec, engine=P.ENGINE_GRID)
+        s = torch.cuda.current_stream(dev)
+        b.run(s)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            b.run(s)
+            e1.record(s)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        r = b.result_rows()[0]
+        res[D] = (min(ts), int(r["score_bytes"]), int(r["cand_evals"]), int(r["decisions"]))
+        del b
+    (t0, b0, c0, d0), (t1, b1, c1, d1) = res[32], res[160]
+    dt = (t1 - t0) / (d1 - d0)
+    bpd = (b1 - b0) / (d1 - d0)
+    ach = bpd / dt / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+            "traffic": None, "peak_source": peak_src, "kernel": "grid_engine (h_DTR)",
+            "workload": f"config5s random locality DAG n={n}, B=0.98*peak_total",
+            "pool_per_decision": (c1 - c0) / (d1 - d0), "bytes_per_decision": bpd, "us_per_decision": dt * 1e6,
+            "decisions_per_s": 1.0 / dt}
+
+
+if __name__ == "__main__":
+    main()

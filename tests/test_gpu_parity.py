@@ -1,0 +1,281 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (north_star): bit-identical eviction traces, rows (status, clock,
+decisions, remats, computations, peak M, trace hash) on every config.
+Everything here is integer: comparisons are exact equality.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from dtr_inputs import LogView, models
+
+pytestmark = pytest.mark.gpu
+
+ROW_FIELDS = ("status", "records_done", "clock", "base", "decisions", "remats", "computations", "peak_M",
+              "trace_hash")
+HS = ["dtr", "dtr_eq", "lru", "size", "msps", "local", "random"]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2006_09616_b200 as P
+    return P
+
+
+def oracle_runs(O, logs, specs, trace=True):
+    out = []
+    for s in specs:
+        r, tr = O.replay(logs[s["log"]], O.HEURISTICS[s["h"]], s["budget"], seed=s.get("seed", 0),
+                         thrash_kill=s.get("thrash_kill", 16), max_decisions=s.get("max_decisions", 0),
+                         trace_cap=(1 << 22) if trace else 0)
+        out.append((r, tr))
+    return out
+
+
+def gpu_batch(P, logs, specs, engine, trace_caps):
+    spec2 = [dict(log=s["log"], budget=s["budget"], heuristic=P.HEURISTICS[s["h"]], seed=s.get("seed", 0),
+                  thrash_kill=s.get("thrash_kill", 16), max_decisions=s.get("max_decisions", 0)) for s in specs]
+    b = P.DeviceBatch(logs, spec2, engine=engine, trace_caps=trace_caps)
+    b.run()
+    import torch
+    torch.cuda.synchronize()
+    rows = b.result_rows()
+    tr = b.traces()
+    return rows, [b.cell_trace(i, tr) if tr is not None else None for i in range(len(specs))]
+
+
+def assert_parity(P, O, logs, specs, engine, check_trace=True):
+    ref = oracle_runs(O, logs, specs, trace=check_trace)
+    caps = [int(r["decisions"]) + 4 if check_trace else 0 for r, _ in ref]
+    rows, trs = gpu_batch(P, logs, specs, engine, caps)
+    for i, ((r, tr), g) in enumerate(zip(ref, rows)):
+        for f in ROW_FIELDS:
+            assert int(g[f]) == int(r[f]), (i, specs[i], f, int(g[f]), int(r[f]))
+        if check_trace:
+            gt = trs[i][: int(g["n_trace"])]
+            assert int(g["n_trace"]) == int(r["decisions"])
+            assert gt.tobytes() == tr.tobytes(), (i, specs[i])
+    return rows
+
+
+# ------------------------------------------------------------------ config 1
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_linear_config1(P, oracle_mod, engine):
+    N = 64
+    B = 2 * math.ceil(math.sqrt(N))
+    logs = [models.linear(N)]
+    specs = [dict(log=0, h=h, budget=B, thrash_kill=0) for h in HS]
+    rows = assert_parity(P, oracle_mod, logs, specs, engine)
+    assert int(rows[0]["clock"]) == 177 and int(rows[0]["decisions"]) == 161
+
+
+# ------------------------------------------------------------------ random programs (edge-heavy)
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_random_programs(P, oracle_mod, engine):
+    logs, specs = [], []
+    for s in range(24 if engine == 1 else 6):
+        w = models.random_program(60, seed=1000 + s, p_release=0.3, max_parents=4)
+        logs.append(w)
+        v = LogView(w)
+        for fr in (0.3, 0.5, 0.8):
+            for h in HS:
+                specs.append(dict(log=len(logs) - 1, h=h, budget=max(3, int(v.peak_live * fr)), seed=s))
+    assert_parity(P, oracle_mod, logs, specs, engine)
+
+
+def test_random_programs_wide(P, oracle_mod):
+    """High fan-in (many distinct adjacent components: exercises the dedup fallback)."""
+    logs, specs = [], []
+    for s in range(12):
+        w = models.random_program(120, seed=2000 + s, p_release=0.2, max_parents=12, window=24)
+        logs.append(w)
+        v = LogView(w)
+        for fr in (0.3, 0.6):
+            for h in ("dtr", "dtr_eq", "msps"):
+                specs.append(dict(log=len(logs) - 1, h=h, budget=max(3, int(v.peak_live * fr))))
+    assert_parity(P, oracle_mod, logs, specs, 1)
+
+
+# ------------------------------------------------------------------ config 2 / 3
+
+def sweep_specs(v, hs, permilles, log=0, **kw):
+    return [dict(log=log, h=h, budget=v.budget(pm), **kw) for h in hs for pm in permilles]
+
+
+def test_resnet32_sweep(P, oracle_mod):
+    w = models.resnet32()
+    v = LogView(w)
+    specs = sweep_specs(v, ["dtr", "dtr_eq", "lru", "size", "msps"], models.sweep_permilles(30))
+    assert_parity(P, oracle_mod, [w], specs, 1)
+
+
+@pytest.mark.parametrize("model", ["densenet100", "unet"])
+def test_config3_subset(P, oracle_mod, model):
+    w = models.CONFIG_MODELS[model]()
+    v = LogView(w)
+    specs = sweep_specs(v, ["dtr", "dtr_eq", "lru", "size", "msps"], [100, 300, 500, 800, 1000])
+    assert_parity(P, oracle_mod, [w], specs, 1)
+
+
+@pytest.mark.parametrize("model", ["transformer", "lstm", "treelstm"])
+def test_long_logs_decision_sample(P, oracle_mod, model):
+    """Config 4/5 shapes at full size: the first K decisions (bounded sample the
+    oracle finishes in seconds), CTA and grid engines."""
+    w = models.CONFIG_MODELS[model]()
+    v = LogView(w)
+    specs = [dict(log=0, h=h, budget=v.budget(pm), max_decisions=300) for h in ("dtr", "dtr_eq", "lru", "msps")
+             for pm in (200, 600)]
+    assert_parity(P, oracle_mod, [w], specs, 1)
+    assert_parity(P, oracle_mod, [w], specs[:4], 2)
+
+
+def test_stress_pool_grid(P, oracle_mod):
+    """Config 5s shape (random locality DAG) on the grid engine, first decisions."""
+    w = models.random_dag(200000, seed=3)
+    v = LogView(w)
+    specs = [dict(log=0, h=h, budget=v.peak_total * 98 // 100, max_decisions=50) for h in ("dtr", "dtr_eq", "lru")]
+    assert_parity(P, oracle_mod, [w], specs, 2)
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_edge_statuses(P, oracle_mod):
+    from dtr_inputs import LogBuilder
+    logs, specs = [], []
+    w = models.linear(16)
+    logs.append(w)
+    specs += [dict(log=0, h="dtr", budget=2, thrash_kill=0),          # OOM
+              dict(log=0, h="size", budget=4, thrash_kill=2),         # thrash kill
+              dict(log=0, h="dtr", budget=4, max_decisions=5)]        # decision cap
+    b = LogBuilder()                                                  # empty log
+    logs.append(b.build())
+    specs.append(dict(log=1, h="dtr", budget=10))
+    b = LogBuilder()                                                  # single tensor, budget below its size
+    b.make(5, 1, [])
+    logs.append(b.build())
+    specs.append(dict(log=2, h="dtr", budget=3))
+    bad = models.linear(8).copy()                                     # malformed: RELEASE twice -> PRECOND
+    v = LogView(bad)
+    ops = v.ops.copy()
+    rel = [i for i, x in enumerate(ops) if (int(x) >> 29) == 3]
+    ops[rel[1]] = ops[rel[0]]
+    bad[len(bad) - len(ops):] = ops
+    logs.append(bad)
+    specs.append(dict(log=3, h="dtr", budget=100))
+    rows = assert_parity(P, oracle_mod, logs, specs, 1)
+    assert [int(r["status"]) for r in rows] == [3, 4, 8, 0, 3, 2]
+
+
+def test_host_e2e_entry(P, oracle_mod):
+    w = models.resnet32()
+    v = LogView(w)
+    words, offs = P.pack_logs([w])
+    specs = [dict(log=0, budget=v.budget(pm), heuristic=P.HEURISTICS[h]) for h in ("dtr", "lru") for pm in
+             (200, 500, 900)]
+    cells, _ = P.make_cells(offs, specs)
+    rows, _ = P.replay_batch_host(words, cells)
+    for i, s in enumerate(specs):
+        r, _ = oracle_mod.replay(w, s["heuristic"], s["budget"])
+        for f in ROW_FIELDS:
+            assert int(rows[i][f]) == int(r[f])
+
+
+def test_determinism(P):
+    w = models.densenet100()
+    v = LogView(w)
+    specs = [dict(log=0, budget=v.budget(pm), heuristic=P.HEURISTICS[h]) for h in ("dtr", "dtr_eq") for pm in
+             (200, 600)]
+    words, offs = P.pack_logs([w])
+    cells, _ = P.make_cells(offs, specs)
+    a, _ = P.replay_batch_host(words, cells)
+    b, _ = P.replay_batch_host(words, cells)
+    assert a.tobytes() == b.tobytes()
+
+
+# ------------------------------------------------------------------ per-call API (fixtures)
+
+def percall_fixture(P, h, parents, evict, mems=None):
+    rt = P.Runtime(P.HEURISTICS[h])
+    for i, ps in enumerate(parents):
+        rc, t = rt.compute(mems[i] if mems else 1, 1, ps)
+        assert rc == 0 and t == i
+    for t in evict:
+        assert rt.debug_evict(t) == 0
+    return rt
+
+
+def test_percall_hand_fixtures(P):
+    import json, os
+    from fractions import Fraction
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hdtr_T_B_clock7.json")))
+    rt = percall_fixture(P, "dtr", g["parents"], g["evict"])
+    sc = {str(k): Fraction(n, d) for k, (n, d) in rt.scores().items()}
+    assert sc == {k: Fraction(*v) for k, v in g["expect_scores"].items()}
+    assert rt.release(3) == 0
+    assert rt.scores()[3][0] == 0
+    s0 = g["staleness0"]
+    rt = percall_fixture(P, "dtr", g["parents"], g["evict"])
+    rt.set_budget(s0["budget"])
+    rc, t = rt.compute(1, 1, s0["make_parents"])
+    assert rc == 0
+    tr = rt.trace()
+    assert [[int(r["clock"]), int(r["id"])] for r in tr] == s0["expect_trace"]
+    assert int(rt.stats()["clock"]) == s0["expect_clock"]
+    # MSPS chain
+    rt = P.Runtime(P.HEURISTICS["msps"])
+    rt.compute(1, 2, [])
+    rt.compute(1, 3, [0])
+    rt.compute(4, 1, [1])
+    rt.debug_evict(0)
+    rt.debug_evict(1)
+    assert Fraction(*rt.scores()[2]) == Fraction(6, 4)
+
+
+def test_percall_vs_oracle_random(P, oracle_mod):
+    """Random per-call sessions incl. REMAT of evicted tensors and preconditions."""
+    rng = np.random.default_rng(7)
+    for h in HS:
+        for trial in range(4):
+            B = int(rng.integers(6, 14))
+            g = P.Runtime(P.HEURISTICS[h], budget=B, seed=trial, cap_tensors=256, cap_edges=1024)
+            o = oracle_mod.Runtime(oracle_mod.HEURISTICS[h], budget=B, seed=trial)
+            live = []
+            for step in range(80):
+                r = rng.random()
+                if r < 0.55 or not live:
+                    k = int(rng.integers(0, min(3, len(live)) + 1))
+                    ps = [int(x) for x in rng.choice(live, size=k, replace=False)] if k else []
+                    m, c = int(rng.integers(1, 4)), int(rng.integers(1, 5))
+                    a, b = g.compute(m, c, ps), o.compute(m, c, ps)
+                    assert a == b, (h, trial, step)
+                    if a[0] == 0:
+                        live.append(a[1])
+                elif r < 0.75:
+                    t = int(rng.choice(live))
+                    assert g.release(t) == o.release(t)
+                    live.remove(t)
+                elif r < 0.85:
+                    t = int(rng.integers(0, o.state()["n"] + 2))
+                    assert g.rematerialize(t) == o.rematerialize(t)
+                elif r < 0.9:
+                    t = int(rng.choice(live))
+                    assert g.get(t) == o.get(t)
+                    live.append(t)
+                else:
+                    t = int(rng.choice(live))
+                    assert g.release(t) == o.release(t)      # may hit rho == 0 -> PRECOND on both
+                    if t in live:
+                        live.remove(t)
+                gs, os_ = g.stats(), o.result()
+                for f in ("status", "clock", "decisions", "remats", "computations", "peak_M", "trace_hash"):
+                    assert int(gs[f]) == int(os_[f]), (h, trial, step, f)
+                if int(gs["status"]) != 0:
+                    break
+            assert g.trace().tobytes() == o.trace().tobytes()
