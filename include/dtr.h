@@ -131,14 +131,17 @@ int dtr_batch_workspace_bytes(const uint32_t *dims, uint32_t n_cells, uint32_t e
                               uint64_t *bytes_out);
 
 /* Replay every cell.  d_words: device, packed logs.  d_cells: device, n_cells
- * dtr_cell.  d_dims: device copy of the dims array above (used to place each
- * cell's workspace).  d_ws: device workspace of ws_bytes (contents
- * overwritten).  d_rows: device, n_cells dtr_result (written).  d_trace:
- * device dtr_evict_rec buffer indexed by each cell's trace_offset (may be NULL
- * when every trace_cap is 0).  Asynchronous on `stream` (cudaStream_t, NULL =
+ * dtr_cell.  h_dims: HOST copy of the dims array above (sizes the workspace
+ * and the shared-memory staging of each launch).  d_ws: device workspace of
+ * ws_bytes (contents overwritten; cell regions are placed on the device).
+ * d_rows: device, n_cells dtr_result (written).  d_trace: device
+ * dtr_evict_rec buffer indexed by each cell's trace_offset (may be NULL when
+ * every trace_cap is 0).  Asynchronous on `stream` (cudaStream_t, NULL =
  * legacy default); per-cell failures are reported in the rows.  Returns
- * DTR_E_INVAL / DTR_E_CAPACITY (workspace too small) / DTR_E_CUDA (launch). */
-int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uint32_t *d_dims,
+ * DTR_E_INVAL / DTR_E_CAPACITY (workspace too small) / DTR_E_CUDA (launch).
+ * CTA engine: one launch, one CTA per cell, each simulation's whole state in
+ * shared memory when it fits (<= 200 KiB), else in its workspace region. */
+int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uint32_t *h_dims,
                      uint32_t n_cells, uint32_t engine, void *d_ws, uint64_t ws_bytes,
                      dtr_result *d_rows, dtr_evict_rec *d_trace, void *stream);
 

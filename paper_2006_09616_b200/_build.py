@@ -19,15 +19,19 @@ def nvcc():
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS)
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    """profile=True builds libdtr_prof.so with clock64 phase counters (probes only)."""
+    lib = LIB if not profile else os.path.join(HERE, "libdtr_prof.so")
+    stale = not os.path.exists(lib) or any(os.path.getmtime(d) > os.path.getmtime(lib) for d in DEPS)
     if force or stale:
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp, SRC]
+        tmp = lib + f".tmp{os.getpid()}"
+        cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
+              (["-DDTR_PROFILE"] if profile else []) + ["-o", tmp, SRC]
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+    print(build(force=True, verbose="-v" in sys.argv, profile="--profile" in sys.argv))

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdtr.so")
+LIB_PATH = os.environ.get("DTR_LIB") or os.path.join(HERE, "libdtr.so")   # DTR_LIB: probes only
 
 DTR_OK, DTR_E_INVAL, DTR_E_PRECOND, DTR_E_OOM, DTR_E_THRASH = 0, 1, 2, 3, 4
 DTR_E_CAPACITY, DTR_E_STATE, DTR_E_CUDA, DTR_E_DECISION_CAP = 5, 6, 7, 8
@@ -154,10 +154,11 @@ def workspace_bytes(dims, engine):
     return out.value
 
 
-def replay_batch(d_words, d_cells, d_dims, n_cells, engine, d_ws, ws_bytes, d_rows, d_trace, stream):
-    """dtr_replay_batch on device pointers (ints), asynchronous on `stream` (int handle)."""
-    _check(lib.dtr_replay_batch(d_words, d_cells, d_dims, n_cells, engine, d_ws, ws_bytes, d_rows, d_trace,
-                                stream), "dtr_replay_batch")
+def replay_batch(d_words, d_cells, h_dims, n_cells, engine, d_ws, ws_bytes, d_rows, d_trace, stream):
+    """dtr_replay_batch on device pointers (ints) with host dims (np.uint32),
+    asynchronous on `stream` (int handle)."""
+    _check(lib.dtr_replay_batch(d_words, d_cells, _np_ptr(h_dims), n_cells, engine, d_ws, ws_bytes, d_rows,
+                                d_trace, stream), "dtr_replay_batch")
 
 
 def replay_batch_host(words, cells, engine=0, trace_total=0, stream=None):
@@ -189,7 +190,7 @@ class DeviceBatch:
         dev = self.device
         self.words = torch.from_numpy(words.view(np.int32)).to(dev)
         self.cells = torch.from_numpy(cells.view(np.uint8)).to(dev)
-        self.dims = torch.from_numpy(dims.view(np.int32)).to(dev)
+        self.h_dims = dims
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
         self.rows = torch.zeros(self.n_cells * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
         self.trace_total = ttot
@@ -199,7 +200,7 @@ class DeviceBatch:
 
     def run(self, stream=None):
         s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
-        replay_batch(self.words.data_ptr(), self.cells.data_ptr(), self.dims.data_ptr(), self.n_cells, self.engine,
+        replay_batch(self.words.data_ptr(), self.cells.data_ptr(), self.h_dims, self.n_cells, self.engine,
                      self.ws.data_ptr(), self.ws_bytes, self.rows.data_ptr(),
                      self.trace.data_ptr() if self.trace is not None else None, s.cuda_stream)
 

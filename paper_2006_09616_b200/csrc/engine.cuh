@@ -3,16 +3,26 @@
 // One simulation = the simrd runtime with V2 banishing (PAPER.md Doc A,
 // P:113-373).  Its control (make_tensor / get_internal recursion /
 // release_internal / free / evict) is inherently sequential and runs
-// on ONE leader thread as a resumable state machine with an explicit stack;
-// whenever free() needs a decision the leader hands the pool to its
-// TEAM -- a whole CTA (many small simulations per GPU, one per CTA) or the whole
+// on ONE leader thread as a resumable state machine with an explicit stack
+// (leader.cuh); whenever free() needs a decision the leader hands the
+// pool to its TEAM -- a whole CTA (one small simulation per CTA) or the whole
 // grid (one large simulation per GPU) -- which scores every pool member and
-// reduces the exact (score, id) argmin.  All state lives in device memory.
+// reduces the exact (score, id) argmin (team.cuh).
+//
+// Memory: every array of a simulation is addressed by a 32-bit WORD offset from
+// one base -- the CTA's dynamic shared memory (SM = true: LDS/STS, 32-bit
+// addresses) or the simulation's global workspace (SM = false).  Per-tensor
+// data is array-of-structs so the leader fetches a tensor with one 16-B load:
+//   srec[t] = {mem, cost, par_off, npar}          (static, from the log)
+//   crec[t] = {ch_off, nch}  | linked: {head, -}  (children, built on device)
+//   drec[t] = {state, la, rho, ell}               (dynamic)
+//   state: bit31 material (t.m = T), bit30 computed once (reading C-19),
+//          bits 0..29 label of t's evicted component (h_DTR)
+//   la:    last_access + 1, 0 = -inf (banish_V2)
 //
 // Independent of oracle/ (shares no code with it).
 #pragma once
 #include <stdint.h>
-#include <cooperative_groups.h>
 
 namespace dtr {
 
@@ -21,11 +31,10 @@ typedef unsigned long long u64;
 typedef unsigned __int128 u128;
 
 constexpr u32 NONE = 0xFFFFFFFFu;
-// state word per tensor: bit31 material (t.m = T), bit30 computed at least
-// once (reading C-19), bits 0..29: evicted-component id (h_DTR exact mode).
 constexpr u32 M_BIT = 1u << 31;
 constexpr u32 O_BIT = 1u << 30;
 constexpr u32 COMP_MASK = (1u << 30) - 1;
+constexpr u32 LIVE_BIT = 1u << 31;           // union-find compaction mark (in uf size)
 constexpr u64 CLOCK_LIMIT = 0xFFFFFFFEull;   // reading C-14: la is stored as clock + 1 in u32
 
 enum { H_DTR = 0, H_DTR_EQ = 1, H_LRU = 2, H_SIZE = 3, H_MSPS = 4, H_LOCAL = 5, H_RANDOM = 6 };
@@ -34,9 +43,90 @@ enum { OP_MAKE = 1, OP_GET = 2, OP_RELEASE = 3, OP_REMAT = 4, OP_ENSURE = 5, OP_
 enum { ST_OK = 0, ST_INVAL = 1, ST_PRECOND = 2, ST_OOM = 3, ST_THRASH = 4, ST_CAPACITY = 5,
        ST_STATE = 6, ST_DECISION_CAP = 8 };
 
-__host__ __device__ inline bool is_evicted(u32 s) { return (s & (M_BIT | O_BIT)) == O_BIT; }
-__host__ __device__ inline bool is_material(u32 s) { return (s & M_BIT) != 0; }
-__host__ __device__ inline u64 align16(u64 x) { return (x + 15) & ~15ull; }
+__host__ __device__ __forceinline__ bool is_evicted(u32 s) { return (s & (M_BIT | O_BIT)) == O_BIT; }
+__host__ __device__ __forceinline__ bool is_material(u32 s) { return (s & M_BIT) != 0; }
+
+// ---------------------------------------------------------------------------
+// Layout: word offsets of every array of one simulation.
+// ---------------------------------------------------------------------------
+struct Lay {
+  u32 n, E, heur, linked;
+  u32 srec, crec, par, ch, drec, pool_ids, pool_pos, fr, pb;
+  u32 mem_next, comp, comp_head, bfs_q, stamp;         // h_DTR (comp rec: {cost lo, cost hi, maxla, size})
+  u32 node_of, uf, uf_size, uf_cap;                    // h_DTR_eq (uf rec: {cost lo, cost hi, maxla, parent})
+  u32 msps_bm, msps_q, msps_words, msps_warps;         // h_MSPS per-warp scratch
+  u32 e_next, e_child;                                 // linked children (per-call)
+  u32 words;                                           // total
+  u32 pad;
+};
+
+// Sizes the workspace (host) and places it (device).  Returns false when the
+// layout does not fit 32-bit word offsets.
+__host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 linked, u32 msps_warps) {
+  u64 o = 0;
+  auto take = [&](u64 words) -> u32 { u64 p = o; o = (o + words + 3) & ~3ull; return (u32)p; };
+  const u64 n1 = (u64)n + 1, e1 = (u64)E + 1;
+  L.n = n; L.E = E; L.heur = heur; L.linked = linked;
+  L.srec = take(4 * n1);
+  L.crec = take(2 * n1);
+  L.par = take(e1);
+  L.ch = linked ? 0 : take(e1);
+  L.drec = take(4 * n1);
+  L.pool_ids = take(n1);
+  L.pool_pos = take(n1);
+  L.fr = take(4 * n1);
+  L.pb = take(e1);
+  L.mem_next = L.comp = L.comp_head = L.bfs_q = L.stamp = 0;
+  L.node_of = L.uf = L.uf_size = L.uf_cap = 0;
+  L.msps_bm = L.msps_q = L.msps_words = L.msps_warps = 0;
+  L.e_next = L.e_child = 0;
+  if (heur == H_DTR) {
+    L.mem_next = take(n1);
+    L.comp = take(4 * n1);
+    L.comp_head = take(n1);
+    L.bfs_q = take(n1);
+    L.stamp = take(n1);
+  } else if (heur == H_DTR_EQ) {
+    L.uf_cap = n + 64;
+    L.node_of = take(n1);
+    L.uf = take(4 * (u64)L.uf_cap);
+    L.uf_size = take(L.uf_cap);
+  } else if (heur == H_MSPS) {
+    L.msps_warps = msps_warps;
+    L.msps_words = (u32)((n1 + 31) / 32);
+    L.msps_bm = take((u64)L.msps_words * msps_warps);
+    L.msps_q = take(n1 * msps_warps);
+  }
+  if (linked) {
+    L.e_next = take(e1);
+    L.e_child = take(e1);
+  }
+  L.words = (u32)o;
+  L.pad = 0;
+  return o < 0xFFFFFFF0ull;
+}
+
+// ---------------------------------------------------------------------------
+// Memory policy: SM -> dynamic shared memory, else a global base pointer.
+// ---------------------------------------------------------------------------
+extern __shared__ __align__(16) u32 g_smem[];
+
+template <bool SM>
+struct Mem {
+  u32 *gbase;
+  __device__ __forceinline__ u32 &w(u32 off) const {
+    if constexpr (SM) return g_smem[off];
+    else return gbase[off];
+  }
+  __device__ __forceinline__ uint4 &q(u32 off) const {   // off multiple of 4
+    if constexpr (SM) return reinterpret_cast<uint4 *>(g_smem)[off >> 2];
+    else return reinterpret_cast<uint4 *>(gbase)[off >> 2];
+  }
+  __device__ __forceinline__ uint2 &d(u32 off) const {   // off multiple of 2
+    if constexpr (SM) return reinterpret_cast<uint2 *>(g_smem)[off >> 1];
+    else return reinterpret_cast<uint2 *>(gbase)[off >> 1];
+  }
+};
 
 // ---------------------------------------------------------------------------
 // Scalars of one simulation (leader state; persisted in device memory between
@@ -52,130 +142,15 @@ struct Scalars {
   u32 thrash_kill;
   u32 records_done;
   u32 sp, pb_top;     // explicit get_internal stack
-  u32 comp_free_top;  // exact components: free-id stack
-  u32 uf_n, uf_cap;   // union-find nodes in use / capacity
-  u32 epoch;
+  u32 uf_n;           // union-find nodes in use
+  u32 epoch;          // BFS stamps
   u32 edges_used;     // linked children (per-call mode)
   u32 cell_id;
   u32 last_rc;        // per-call: result code of the last op
   u32 pending_op;     // per-call: the op word being applied
   u32 n_scores;       // per-call OP_SCORES: pool size scored
-  u32 pad[3];
+  u32 pad[5];
 };
-
-// ---------------------------------------------------------------------------
-// Read-only graph of a log: tensor table + parents CSR (from the log) and the
-// children lists built on the device.
-// ---------------------------------------------------------------------------
-struct Graph {
-  u32 n, E, nops;
-  const u32 *mem, *cost, *par_off, *par, *ops;
-  u64 base;
-  // children: CSR (batch) or linked lists (per-call)
-  u32 linked;
-  u32 *ch_off, *ch;                     // CSR: ch[ch_off[p] .. ch_off[p+1])
-  u32 *ch_head, *e_next, *e_child;      // linked: e = ch_head[p]; e != NONE; e = e_next[e]
-};
-
-__host__ __device__ inline void graph_from_log(Graph &g, const u32 *w) {
-  g.n = w[2]; g.E = w[3]; g.nops = w[4];
-  g.base = (u64)w[6] | ((u64)w[7] << 32);
-  g.mem = w + 16;
-  g.cost = g.mem + g.n;
-  g.par_off = g.cost + g.n;
-  g.par = g.par_off + g.n + 1;
-  g.ops = g.par + g.E;
-  g.linked = 0;
-}
-
-// ---------------------------------------------------------------------------
-// Per-simulation mutable state (structure of arrays in device memory).
-// ---------------------------------------------------------------------------
-struct Work {
-  Scalars *sc;
-  u32 *state, *la, *rho, *ell, *pool_ids, *pool_pos;
-  u32 *fr_t, *fr_base, *fr_cnt, *fr_next, *pb;
-  // exact evicted components (h_DTR)
-  u64 *comp_cost;
-  u32 *comp_maxla, *comp_head, *comp_size, *mem_next, *comp_free, *bfs_q, *stamp;
-  // union-find (h_DTR_eq)
-  u32 *node_of, *uf_parent, *uf_maxla, *uf_size, *uf_remap, *uf_roots, *uf_tmaxla, *uf_tsize;
-  u64 *uf_cost, *uf_tcost;
-  // children CSR scratch (batch) / linked lists (per-call)
-  u32 *ch_off, *ch, *ch_fill;
-  u32 *ch_head, *e_next, *e_child;
-  // MSPS per-warp scratch
-  u32 *msps_bm, *msps_q;
-  u32 msps_words;
-};
-
-// Carve the workspace of one simulation.  Same function sizes it on the host
-// (base = 0) and places it on the device.  Arrays unused by the heuristic get
-// no space.
-__host__ __device__ inline u64 carve(Work &w, uintptr_t base, u32 n, u32 E, u32 heur, u32 linked,
-                                      u32 msps_warps) {
-  u64 off = 0;
-  auto take = [&](u64 bytes) -> uintptr_t { uintptr_t p = base + off; off = align16(off + bytes); return p; };
-  u64 n1 = (u64)n + 1;
-  w.sc = (Scalars *)take(sizeof(Scalars));
-  w.state = (u32 *)take(4 * n1);
-  w.la = (u32 *)take(4 * n1);
-  w.rho = (u32 *)take(4 * n1);
-  w.ell = (u32 *)take(4 * n1);
-  w.pool_ids = (u32 *)take(4 * n1);
-  w.pool_pos = (u32 *)take(4 * n1);
-  w.fr_t = (u32 *)take(4 * n1);
-  w.fr_base = (u32 *)take(4 * n1);
-  w.fr_cnt = (u32 *)take(4 * n1);
-  w.fr_next = (u32 *)take(4 * n1);
-  w.pb = (u32 *)take(4 * ((u64)E + 1));
-  w.comp_cost = nullptr; w.comp_maxla = w.comp_head = w.comp_size = w.mem_next = w.comp_free = nullptr;
-  w.bfs_q = w.stamp = nullptr;
-  if (heur == H_DTR) {
-    w.comp_cost = (u64 *)take(8 * n1);
-    w.comp_maxla = (u32 *)take(4 * n1);
-    w.comp_head = (u32 *)take(4 * n1);
-    w.comp_size = (u32 *)take(4 * n1);
-    w.mem_next = (u32 *)take(4 * n1);
-    w.comp_free = (u32 *)take(4 * n1);
-    w.bfs_q = (u32 *)take(4 * n1);
-    w.stamp = (u32 *)take(4 * n1);
-  }
-  w.node_of = w.uf_parent = w.uf_maxla = w.uf_size = w.uf_remap = w.uf_roots = w.uf_tmaxla = w.uf_tsize = nullptr;
-  w.uf_cost = w.uf_tcost = nullptr;
-  if (heur == H_DTR_EQ) {
-    u64 cap = 2 * (u64)n + 64;
-    w.node_of = (u32 *)take(4 * n1);
-    w.uf_parent = (u32 *)take(4 * cap);
-    w.uf_maxla = (u32 *)take(4 * cap);
-    w.uf_size = (u32 *)take(4 * cap);
-    w.uf_remap = (u32 *)take(4 * cap);
-    w.uf_roots = (u32 *)take(4 * cap);
-    w.uf_tmaxla = (u32 *)take(4 * cap);
-    w.uf_tsize = (u32 *)take(4 * cap);
-    w.uf_cost = (u64 *)take(8 * cap);
-    w.uf_tcost = (u64 *)take(8 * cap);
-  }
-  w.msps_bm = w.msps_q = nullptr;
-  w.msps_words = 0;
-  if (heur == H_MSPS) {
-    // MSPS closure scratch, one per scoring warp: visited bitmap + BFS queue
-    w.msps_words = (u32)((n1 + 31) / 32);
-    w.msps_bm = (u32 *)take(4 * (u64)w.msps_words * msps_warps);
-    w.msps_q = (u32 *)take(4 * n1 * msps_warps);
-  }
-  w.ch_off = w.ch = w.ch_fill = w.ch_head = w.e_next = w.e_child = nullptr;
-  if (!linked) {
-    w.ch_off = (u32 *)take(4 * (n1 + 1));
-    w.ch = (u32 *)take(4 * ((u64)E + 1));
-    w.ch_fill = (u32 *)take(4 * n1);
-  } else {
-    w.ch_head = (u32 *)take(4 * n1);
-    w.e_next = (u32 *)take(4 * ((u64)E + 1));
-    w.e_child = (u32 *)take(4 * ((u64)E + 1));
-  }
-  return off;
-}
 
 // ---------------------------------------------------------------------------
 // Exact rational scores.  den == 0 encodes +infinity.
@@ -185,9 +160,29 @@ struct Cand {
   u32 id;
 };
 
+// a.num * b.den < b.num * a.den, exactly.  Numerators are < 2^32 for every
+// heuristic but h_random (whose den is 1): then each product is a 32 x 64-bit
+// product compared as (high 64, low 32); else full 128-bit products.
+__device__ __forceinline__ bool score_less(const Cand &a, const Cand &b) {
+  if (((a.num | b.num) >> 32) == 0) {
+    const u32 an = (u32)a.num, bn = (u32)b.num;
+    const u64 l0 = (u64)an * (u32)b.den, l1 = (u64)an * (u32)(b.den >> 32);
+    const u64 r0 = (u64)bn * (u32)a.den, r1 = (u64)bn * (u32)(a.den >> 32);
+    const u64 lh = l1 + (l0 >> 32), rh = r1 + (r0 >> 32);
+    if (lh != rh) return lh < rh;
+    return (u32)l0 < (u32)r0;
+  }
+  return (u128)a.num * b.den < (u128)b.num * a.den;
+}
+
+__device__ __forceinline__ bool score_eq(const Cand &a, const Cand &b) {
+  return !score_less(a, b) && !score_less(b, a);
+}
+
+// lexicographic (score, id): equal scores -> smaller id (reading C-5)
 __device__ __forceinline__ bool cand_less(const Cand &a, const Cand &b) {
-  u128 l = (u128)a.num * b.den, r = (u128)b.num * a.den;
-  if (l != r) return l < r;
+  if (score_less(a, b)) return true;
+  if (score_less(b, a)) return false;
   return a.id < b.id;
 }
 
@@ -210,146 +205,47 @@ __device__ __forceinline__ void stale_score(u64 num, u32 mem, u32 L_enc, u64 clo
   on = num; od = (u64)mem * s;
 }
 
-// ---------------------------------------------------------------------------
-// Neighbour iteration: parents (log CSR) then visible children.
-// ---------------------------------------------------------------------------
-template <class F>
-__device__ __forceinline__ void for_each_nbr(const Graph &g, u32 t, F f) {
-  u32 b = __ldg(&g.par_off[t]), e = __ldg(&g.par_off[t + 1]);
-  for (u32 j = b; j < e; j++) f(__ldg(&g.par[j]));
-  if (!g.linked) {
-    u32 cb = g.ch_off[t], ce = g.ch_off[t + 1];
-    for (u32 j = cb; j < ce; j++) f(g.ch[j]);
-  } else {
-    for (u32 x = g.ch_head[t]; x != NONE; x = g.e_next[x]) f(g.e_child[x]);
-  }
-}
+__device__ __forceinline__ u64 mk64(u32 lo, u32 hi) { return (u64)lo | ((u64)hi << 32); }
 
-// union-find find without compression (read-only: used inside the parallel score pass)
-__device__ __forceinline__ u32 uf_find_ro(const u32 *parent, u32 x) {
-  u32 p = parent[x];
-  while (p != x) { x = p; p = parent[x]; }
-  return x;
-}
+// ---------------------------------------------------------------------------
+// Graph access shared by the leader and the team.
+// ---------------------------------------------------------------------------
+template <bool SM>
+struct Sim {
+  Mem<SM> m;
+  Lay L;
 
-// Sum of component costs over DISTINCT evicted components adjacent to t and the
-// max of their la (h_DTR: exact labels; h_DTR_eq: UF roots).  Dedup: the last
-// four distinct ids are kept in registers; beyond that an earlier-neighbour
-// rescan decides.
-// Algorithmic bytes: each neighbour costs its id + state
-// word (8 B); each distinct component its cost + maxla (12 B); h_DTR_eq adds
-// node_of (4 B) per evicted neighbour and 4 B per union-find parent step.
-template <bool UF>
-__device__ __forceinline__ void nbr_components(const Graph &g, const Work &w, u32 t, u64 &sum, u32 &L,
-                                               u64 &bytes) {
-  u32 c0 = NONE, c1 = NONE, c2 = NONE, c3 = NONE, nd = 0;
-  u32 nb = 0, extra = 0;
-  auto comp_of = [&](u32 q, u32 sq) -> u32 {
-    if (UF) {
-      u32 x = w.node_of[q], p = w.uf_parent[x];
-      extra += 8;
-      while (p != x) { x = p; p = w.uf_parent[x]; extra += 4; }
-      return x;
+  __device__ __forceinline__ uint4 &srec(u32 t) const { return m.q(L.srec + 4 * t); }
+  __device__ __forceinline__ uint2 &crec(u32 t) const { return m.d(L.crec + 2 * t); }
+  __device__ __forceinline__ uint4 &drec(u32 t) const { return m.q(L.drec + 4 * t); }
+  __device__ __forceinline__ u32 &state(u32 t) const { return m.w(L.drec + 4 * t); }
+  __device__ __forceinline__ u32 &la(u32 t) const { return m.w(L.drec + 4 * t + 1); }
+  __device__ __forceinline__ u32 &rho(u32 t) const { return m.w(L.drec + 4 * t + 2); }
+  __device__ __forceinline__ u32 &ell(u32 t) const { return m.w(L.drec + 4 * t + 3); }
+  __device__ __forceinline__ u32 &par(u32 j) const { return m.w(L.par + j); }
+  __device__ __forceinline__ u32 &pool_ids(u32 i) const { return m.w(L.pool_ids + i); }
+  __device__ __forceinline__ u32 &pool_pos(u32 t) const { return m.w(L.pool_pos + t); }
+  __device__ __forceinline__ uint4 &comp(u32 c) const { return m.q(L.comp + 4 * c); }
+  __device__ __forceinline__ uint4 &uf(u32 x) const { return m.q(L.uf + 4 * x); }
+
+  // parents of t (srec already loaded) then children
+  template <class F>
+  __device__ __forceinline__ void for_each_nbr(u32 t, const uint4 &sr, F f) const {
+    for (u32 j = 0; j < sr.w; j++) f(par(sr.z + j));
+    uint2 cr = crec(t);
+    if (!L.linked) {
+      for (u32 j = 0; j < cr.y; j++) f(m.w(L.ch + cr.x + j));
+    } else {
+      for (u32 e = cr.x; e != NONE; e = m.w(L.e_next + e)) f(m.w(L.e_child + e));
     }
-    return sq & COMP_MASK;
-  };
-  auto seen_earlier = [&](u32 upto_q_pos, u32 c) -> bool {
-    // rescan neighbours at positions < upto_q_pos
-    u32 pos = 0; bool found = false;
-    for_each_nbr(g, t, [&](u32 y) {
-      if (found || pos >= upto_q_pos) { pos++; return; }
-      pos++;
-      u32 sy = w.state[y];
-      if (is_evicted(sy) && comp_of(y, sy) == c) found = true;
-    });
-    return found;
-  };
-  u32 pos = 0;
-  for_each_nbr(g, t, [&](u32 q) {
-    u32 my = pos++;
-    nb++;
-    u32 sq = w.state[q];
-    if (!is_evicted(sq)) return;
-    u32 c = comp_of(q, sq);
-    if (c == c0 || c == c1 || c == c2 || c == c3) return;
-    if (nd >= 4 && seen_earlier(my, c)) return;
-    nd++;
-    c3 = c2; c2 = c1; c1 = c0; c0 = c;
-    if (UF) { sum += w.uf_cost[c]; u32 m = w.uf_maxla[c]; L = m > L ? m : L; }
-    else { sum += w.comp_cost[c]; u32 m = w.comp_maxla[c]; L = m > L ? m : L; }
-  });
-  bytes += 8ull * nb + 12ull * nd + extra;
-}
-
-// score of one pool member (MSPS handled separately: it needs per-candidate scratch)
-// bytes: algorithmic bytes this candidate's score reads, pool id included.
-__device__ __forceinline__ void score_one(const Graph &g, const Work &w, u32 heur, u64 clock, u64 seed,
-                                          u64 decisions, u32 t, u64 &num, u64 &den, u64 &bytes) {
-  switch (heur) {
-    case H_DTR: {
-      u64 sum = 0; u32 L = w.la[t];
-      nbr_components<false>(g, w, t, sum, L, bytes);
-      stale_score((u64)__ldg(&g.cost[t]) + sum, __ldg(&g.mem[t]), L, clock, num, den);
-      bytes += 4 + 12 + 16;   // pool id; mem, cost, la; parent + child CSR offsets
-      return;
-    }
-    case H_DTR_EQ: {
-      u64 sum = 0; u32 L = w.la[t];
-      nbr_components<true>(g, w, t, sum, L, bytes);
-      stale_score((u64)__ldg(&g.cost[t]) + sum, __ldg(&g.mem[t]), L, clock, num, den);
-      bytes += 4 + 12 + 16;
-      return;
-    }
-    case H_LRU:
-      stale_score(1, 1, w.la[t], clock, num, den);
-      bytes += 8;
-      return;
-    case H_SIZE:
-      num = 1; den = __ldg(&g.mem[t]);
-      bytes += 8;
-      return;
-    case H_LOCAL:
-      stale_score((u64)__ldg(&g.cost[t]), __ldg(&g.mem[t]), w.la[t], clock, num, den);
-      bytes += 16;
-      return;
-    case H_RANDOM:
-      num = splitmix64(seed ^ (decisions << 32) ^ (u64)t); den = 1;
-      bytes += 4;
-      return;
   }
-  num = 0; den = 1;
-}
 
-// ---------------------------------------------------------------------------
-// Reductions
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ Cand warp_argmin(Cand c) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    Cand d;
-    d.num = __shfl_xor_sync(0xffffffffu, c.num, o);
-    d.den = __shfl_xor_sync(0xffffffffu, c.den, o);
-    d.id = __shfl_xor_sync(0xffffffffu, c.id, o);
-    if (cand_less(d, c)) c = d;
+  // union-find find without compression (read-only: safe inside the parallel score pass)
+  __device__ __forceinline__ u32 uf_root(u32 x, u32 &steps) const {
+    u32 p = uf(x).w;
+    while (p != x) { x = p; p = uf(x).w; steps++; }
+    return x;
   }
-  return c;
-}
-
-struct RedSmem {
-  Cand warp[32];
 };
-
-// block-wide argmin; the result is valid in warp 0 (all lanes) after return.
-__device__ __forceinline__ Cand block_argmin(Cand c, RedSmem &sm) {
-  c = warp_argmin(c);
-  u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  if (lane == 0) sm.warp[wid] = c;
-  __syncthreads();
-  if (wid == 0) {
-    c = lane < nw ? sm.warp[lane] : cand_none();
-    c = warp_argmin(c);
-  }
-  return c;
-}
 
 }  // namespace dtr

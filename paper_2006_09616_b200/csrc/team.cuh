@@ -1,0 +1,375 @@
+// team.cuh -- K3 (score pass) + K4 (argmin) + K5 (MSPS closure) of one
+// eviction decision, run by a whole team (CTA or grid) over the pool.
+//
+// score(t) per heuristic (exact rationals, den == 0 = +inf):
+//   h_DTR     (c0(t) + sum over the DISTINCT evicted components adjacent to t of
+//              their cost) / (m(t) * (clock - max(la(t), their max la)))
+//   h_DTR_eq  same with union-find roots (no unions while querying)
+//   h_LRU     1 / s(t)
+//   h_size    1 / m(t)
+//   h_MSPS    (c0(t) + sum_{e_R(t)} c0) / m(t)
+//   h_local   c0(t) / (m(t) s(t))
+//   h_random  splitmix64(seed ^ decision << 32 ^ t)                        P:1269 (C-15)
+// Algorithmic bytes per candidate are counted as they are read (DESIGN.md
+// "Roofline"): pool id 4, static record 16, la 4, children record 8, then 8
+// per neighbour (id + state word), 12 per distinct component (cost + max la),
+// h_DTR_eq +4 per evicted neighbour (node id) and +4 per union-find step.
+#pragma once
+#include "engine.cuh"
+#include "leader.cuh"
+
+namespace dtr {
+
+// Distinct adjacent evicted components: the last four labels are kept in
+// registers; beyond four an earlier-neighbour rescan decides duplicates.
+template <bool SM, bool UF>
+__device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const uint4 &sr, u64 &sum, u32 &L,
+                                               u64 &bytes) {
+  u32 c0 = NONE, c1 = NONE, c2 = NONE, c3 = NONE, nd = 0, nb = 0, extra = 0;
+  auto comp_of = [&](u32 q, u32 sq, u32 &steps) -> u32 {
+    if constexpr (UF) return g.uf_root(g.m.w(g.L.node_of + q), steps);
+    else return sq & COMP_MASK;
+  };
+  u32 pos = 0;
+  g.for_each_nbr(t, sr, [&](u32 q) {
+    const u32 my = pos++;
+    nb++;
+    const u32 sq = g.state(q);
+    if (!is_evicted(sq)) return;
+    u32 steps = 0;
+    const u32 c = comp_of(q, sq, steps);
+    if constexpr (UF) extra += 4 + 4 * steps;
+    if (c == c0 || c == c1 || c == c2 || c == c3) return;
+    if (nd >= 4) {
+      u32 p2 = 0;
+      bool dup = false;
+      g.for_each_nbr(t, sr, [&](u32 y) {
+        if (dup || p2 >= my) { p2++; return; }
+        p2++;
+        u32 sy = g.state(y), st2 = 0;
+        if (is_evicted(sy) && comp_of(y, sy, st2) == c) dup = true;
+      });
+      if (dup) return;
+    }
+    nd++;
+    c3 = c2; c2 = c1; c1 = c0; c0 = c;
+    uint4 cr = UF ? g.uf(c) : g.comp(c);
+    sum += mk64(cr.x, cr.y);
+    L = cr.z > L ? cr.z : L;
+  });
+  bytes += 8ull * nb + 12ull * nd + extra;
+}
+
+template <bool SM>
+__device__ __forceinline__ void score_one(const Sim<SM> &g, u32 heur, u64 clock, u64 seed, u64 decisions, u32 t,
+                                          u64 &num, u64 &den, u64 &bytes) {
+  switch (heur) {
+    case H_DTR: {
+      const uint4 sr = g.srec(t);
+      u64 sum = 0;
+      u32 L = g.la(t);
+      nbr_components<SM, false>(g, t, sr, sum, L, bytes);
+      stale_score((u64)sr.y + sum, sr.x, L, clock, num, den);
+      bytes += 4 + 16 + 4 + 8;
+      return;
+    }
+    case H_DTR_EQ: {
+      const uint4 sr = g.srec(t);
+      u64 sum = 0;
+      u32 L = g.la(t);
+      nbr_components<SM, true>(g, t, sr, sum, L, bytes);
+      stale_score((u64)sr.y + sum, sr.x, L, clock, num, den);
+      bytes += 4 + 16 + 4 + 8;
+      return;
+    }
+    case H_LRU:
+      stale_score(1, 1, g.la(t), clock, num, den);
+      bytes += 8;
+      return;
+    case H_SIZE:
+      num = 1; den = g.srec(t).x;
+      bytes += 8;
+      return;
+    case H_LOCAL: {
+      const uint4 sr = g.srec(t);
+      stale_score((u64)sr.y, sr.x, g.la(t), clock, num, den);
+      bytes += 4 + 16 + 4;
+      return;
+    }
+    case H_RANDOM:
+      num = splitmix64(seed ^ (decisions << 32) ^ (u64)t); den = 1;
+      bytes += 4;
+      return;
+  }
+  num = 0; den = 1;
+}
+
+// K5: warp-cooperative e_R(t) -- evicted ancestors reached through evicted
+// parents.  Per-warp visited bitmap + queue; the sum of their c0
+// is returned in every lane.
+template <bool SM>
+__device__ u64 msps_closure(const Sim<SM> &g, u32 t, u32 wslot, volatile u32 *tail, u64 &bytes) {
+  const u32 lane = threadIdx.x & 31;
+  const u32 bm = g.L.msps_bm + wslot * g.L.msps_words;
+  const u32 q = g.L.msps_q + wslot * (g.L.n + 1);
+  if (lane == 0) *tail = 0;
+  __syncwarp();
+  u64 sum = 0;
+  auto visit = [&](u32 p) {
+    bytes += 8;   // parent id + its state word
+    if (!is_evicted(g.state(p))) return;
+    u32 bit = 1u << (p & 31);
+    u32 old = atomicOr(&g.m.w(bm + (p >> 5)), bit);
+    if (old & bit) return;
+    bytes += 16;  // its static record
+    sum += g.srec(p).y;
+    u32 pos = atomicAdd((u32 *)tail, 1u);
+    g.m.w(q + pos) = p;
+  };
+  const uint4 st = g.srec(t);
+  for (u32 j = lane; j < st.w; j += 32) visit(g.par(st.z + j));
+  __syncwarp();
+  u32 head = 0, tl = *tail;
+  __syncwarp();
+  while (head < tl) {
+    for (u32 i = head + lane; i < tl; i += 32) {
+      u32 x = g.m.w(q + i);
+      const uint4 sx = g.srec(x);
+      for (u32 j = 0; j < sx.w; j++) visit(g.par(sx.z + j));
+    }
+    __syncwarp();
+    head = tl;
+    tl = *tail;
+    __syncwarp();
+  }
+  for (u32 i = lane; i < tl; i += 32) g.m.w(bm + (g.m.w(q + i) >> 5)) = 0;
+  __syncwarp();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  return sum;
+}
+
+// ---------------------------------------------------------------------------
+// Exact argmin with a fast path.  key(c) = float(num) / float(den) as monotone
+// u32 bits (0 = score 0, 0x7F800000 = +inf, 0xFFFFFFFF = no candidate).  The
+// computed key of a finite nonzero score has relative error < 6 * 2^-24, so
+// keys more than KEY_MARGIN ulps apart order exactly like the rationals; only
+// keys within the margin (near-ties) are compared exactly in 128 bits.  Scores
+// 0 and +inf are exact classes (ties broken by the smaller id, reading C-5).
+// ---------------------------------------------------------------------------
+constexpr u32 KEY_NONE = 0xFFFFFFFFu, KEY_INF = 0x7F800000u, KEY_MARGIN = 256u;   // 256 ulps >= 2^-16 relative
+
+__device__ __forceinline__ u32 cand_key(const Cand &c) {
+  if (c.id == NONE) return KEY_NONE;
+  if (c.den == 0) return KEY_INF;
+  if (c.num == 0) return 0u;
+  return __float_as_uint(__fdividef(__ull2float_rn(c.num), __ull2float_rn(c.den)));
+}
+
+// best := min(best, c) exactly; bk tracks key(best)
+__device__ __forceinline__ void cand_take(Cand &best, u32 &bk, const Cand &c) {
+  const u32 k = cand_key(c);
+  if (k == KEY_NONE) return;
+  bool better;
+  if (k + KEY_MARGIN < bk) better = true;
+  else if (bk != KEY_NONE && k > bk + KEY_MARGIN) better = false;
+  else better = cand_less(c, best);
+  if (better) { best = c; bk = k; }
+}
+
+__device__ __forceinline__ Cand shfl_cand(const Cand &c, int src) {
+  Cand r;
+  r.num = __shfl_sync(0xffffffffu, c.num, src);
+  r.den = __shfl_sync(0xffffffffu, c.den, src);
+  r.id = __shfl_sync(0xffffffffu, c.id, src);
+  return r;
+}
+
+__device__ __forceinline__ Cand warp_argmin(Cand c);   // exact (below)
+
+// warp-wide exact argmin using the key fast path; every lane gets the result.
+__device__ __forceinline__ Cand warp_argmin_fast(const Cand &c, u32 k) {
+  const u32 FULL = 0xffffffffu;
+  const u32 kmin = __reduce_min_sync(FULL, k);
+  if (kmin == KEY_NONE) return cand_none();
+  if (kmin == 0u || kmin == KEY_INF) {             // exact class: smallest id wins
+    const u32 idmin = __reduce_min_sync(FULL, k == kmin ? c.id : NONE);
+    const u32 m = __ballot_sync(FULL, k == kmin && c.id == idmin);
+    return shfl_cand(c, __ffs(m) - 1);
+  }
+  const bool in = k <= kmin + KEY_MARGIN;
+  const u32 cont = __ballot_sync(FULL, in);
+  if (__popc(cont) == 1) return shfl_cand(c, __ffs(cont) - 1);
+  // near-ties: take the contender with the smallest id as reference; if no
+  // contender's score is strictly below it, it is the exact argmin (exact ties,
+  // the common case for size / LRU); else reduce the strictly-smaller ones exactly
+  const u32 idref = __reduce_min_sync(FULL, in ? c.id : NONE);
+  const Cand ref = shfl_cand(c, __ffs(__ballot_sync(FULL, in && c.id == idref)) - 1);
+  const bool below = in && score_less(c, ref);
+  if (__ballot_sync(FULL, below) == 0) return ref;
+  return warp_argmin(below ? c : cand_none());
+}
+
+// per-heuristic score of pool member t
+template <bool SM, int H>
+__device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t, Cand &c, u64 &bytes) {
+  c.id = t;
+  if constexpr (H == H_DTR || H == H_DTR_EQ) {
+    const uint4 sr = g.srec(t);
+    u64 sum = 0;
+    u32 L = g.la(t);
+    nbr_components<SM, H == H_DTR_EQ>(g, t, sr, sum, L, bytes);
+    stale_score((u64)sr.y + sum, sr.x, L, cmd.clock, c.num, c.den);
+    bytes += 4 + 16 + 4 + 8;
+  } else if constexpr (H == H_LRU) {
+    stale_score(1, 1, g.la(t), cmd.clock, c.num, c.den);
+    bytes += 8;
+  } else if constexpr (H == H_SIZE) {
+    c.num = 1; c.den = g.srec(t).x;
+    bytes += 8;
+  } else if constexpr (H == H_LOCAL) {
+    const uint4 sr = g.srec(t);
+    stale_score((u64)sr.y, sr.x, g.la(t), cmd.clock, c.num, c.den);
+    bytes += 4 + 16 + 4;
+  } else {
+    c.num = splitmix64(cmd.seed ^ (cmd.decisions << 32) ^ (u64)t); c.den = 1;
+    bytes += 4;
+  }
+}
+
+template <bool SM, int H>
+__device__ __forceinline__ void score_loop(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, Cand &best,
+                                           u32 &bk, u64 &bytes, u64 &evals) {
+  const u32 P = cmd.pool_size;
+  u32 i = rank;
+  for (; i + size < P; i += 2 * size) {            // two independent candidates in flight
+    const u32 t0 = g.pool_ids(i), t1 = g.pool_ids(i + size);
+    Cand c0, c1;
+    score_h<SM, H>(g, cmd, t0, c0, bytes);
+    score_h<SM, H>(g, cmd, t1, c1, bytes);
+    cand_take(best, bk, c0);
+    cand_take(best, bk, c1);
+    evals += 2;
+  }
+  if (i < P) {
+    Cand c0;
+    score_h<SM, H>(g, cmd, g.pool_ids(i), c0, bytes);
+    cand_take(best, bk, c0);
+    evals++;
+  }
+}
+
+// Score every pool member of this thread's slice; return the slice argmin and
+// its key.  rank/size: thread index in the team; wrank/wsize: warp index (MSPS).
+template <bool SM>
+__device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, u32 wrank, u32 wsize,
+                           volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk) {
+  Cand best = cand_none();
+  bk = KEY_NONE;
+  switch (cmd.heur) {
+    case H_DTR: score_loop<SM, H_DTR>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_DTR_EQ: score_loop<SM, H_DTR_EQ>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_LRU: score_loop<SM, H_LRU>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_SIZE: score_loop<SM, H_SIZE>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_LOCAL: score_loop<SM, H_LOCAL>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_RANDOM: score_loop<SM, H_RANDOM>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    default: break;
+  }
+  // H_MSPS: one warp per candidate
+  const u32 P = cmd.pool_size;
+  const u32 nw = wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
+  if (wrank >= nw) return best;
+  const u32 lane = threadIdx.x & 31;
+  for (u32 i = wrank; i < P; i += nw) {
+    const u32 t = g.pool_ids(i);
+    const u64 sum = msps_closure(g, t, wrank, msps_tail + (threadIdx.x >> 5), bytes);
+    if (lane == 0) {
+      const uint4 sr = g.srec(t);
+      Cand c;
+      c.num = (u64)sr.y + sum;
+      c.den = sr.x;
+      c.id = t;
+      bytes += 4 + 16;
+      evals++;
+      cand_take(best, bk, c);
+    }
+  }
+  return best;
+}
+
+// per-call OP_SCORES: write every pool member's score (MSPS included)
+template <bool SM>
+__device__ void team_scores_out(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, volatile u32 *msps_tail,
+                                u64 *onum, u64 *oden, u32 *oid) {
+  const u32 P = cmd.pool_size;
+  u64 junk = 0;
+  if (cmd.heur == H_MSPS) {
+    const u32 wr = rank >> 5, ws = (size + 31) >> 5, lane = threadIdx.x & 31;
+    const u32 nw = ws < g.L.msps_warps ? ws : g.L.msps_warps;
+    if (wr >= nw) return;
+    for (u32 i = wr; i < P; i += nw) {
+      const u32 t = g.pool_ids(i);
+      const u64 sum = msps_closure(g, t, wr, msps_tail + (threadIdx.x >> 5), junk);
+      if (lane == 0) { const uint4 sr = g.srec(t); onum[i] = (u64)sr.y + sum; oden[i] = sr.x; oid[i] = t; }
+    }
+    return;
+  }
+  for (u32 i = rank; i < P; i += size) {
+    const u32 t = g.pool_ids(i);
+    u64 num, den;
+    score_one(g, cmd.heur, cmd.clock, cmd.seed, cmd.decisions, t, num, den, junk);
+    onum[i] = num; oden[i] = den; oid[i] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Reductions
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ Cand warp_argmin(Cand c) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand d;
+    d.num = __shfl_xor_sync(0xffffffffu, c.num, o);
+    d.den = __shfl_xor_sync(0xffffffffu, c.den, o);
+    d.id = __shfl_xor_sync(0xffffffffu, c.id, o);
+    if (cand_less(d, c)) c = d;
+  }
+  return c;
+}
+
+struct RedSmem {
+  Cand warp[32];
+};
+
+// block-wide argmin; the result is valid in warp 0 (all lanes) after return.
+__device__ __forceinline__ Cand block_argmin(const Cand &c, u32 k, RedSmem &sm) {
+  Cand w = warp_argmin_fast(c, k);
+  const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) sm.warp[wid] = w;
+  __syncthreads();
+  if (wid == 0) {
+    w = lane < nw ? sm.warp[lane] : cand_none();
+    w = warp_argmin_fast(w, cand_key(w));
+  }
+  return w;
+}
+
+// block-wide sum of two counters; result valid in thread 0
+__device__ __forceinline__ void block_sum2(u64 &a, u64 &b, RedSmem &sm) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) { sm.warp[wid].num = a; sm.warp[wid].den = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = 0; b = 0;
+    for (u32 i = 0; i < nw; i++) { a += sm.warp[i].num; b += sm.warp[i].den; }
+  }
+  __syncthreads();
+}
+
+}  // namespace dtr
