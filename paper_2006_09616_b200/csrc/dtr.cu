@@ -297,14 +297,14 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   if (tid == 0) { row->score_bytes = bytes; row->cand_evals = evals; }
 }
 
-__global__ void __launch_bounds__(CTA_THREADS) cta_engine(const u32 *words, const dtr_cell *cells, u32 n_cells,
+__global__ void __launch_bounds__(CTA_THREADS) cta_engine(const u32 *words, const dtr_cell *cells, u32 c0, u32 n_run,
                                                           char *ws, u64 ws_bytes, dtr_result *rows,
                                                           dtr_evict_rec *trace, u32 smem_bytes) {
   __shared__ CtaShared sh;
   const u32 tid = threadIdx.x;
-  const u32 ci = blockIdx.x;
-  if (ci >= n_cells) return;
-  // this cell's global region: header + sizes of the cells before it
+  if (blockIdx.x >= n_run) return;
+  const u32 ci = c0 + blockIdx.x;
+  // this cell's global region: header + sizes of all cells before it
   u64 part = 0, junk = 0;
   for (u32 j = tid; j < ci; j += blockDim.x) {
     const dtr_cell c = cells[j];
@@ -582,23 +582,62 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
   cudaStream_t st = (cudaStream_t)stream;
   char *ws = (char *)d_ws;
   if (engine == DTR_ENGINE_CTA) {
-    u64 smem = 0;
-    for (u32 i = 0; i < n_cells; i++) {
+    // Consecutive cells of the same shared-memory class form one launch: small
+    // (<= 48 KiB: several CTAs per SM), large (<= 200 KiB staged), global (state
+    // stays in the workspace).  Classes run concurrently on forked streams.
+    static cudaStream_t cls_st[3];
+    static cudaEvent_t fork_ev, join_ev[3];
+    static bool init = false;
+    if (!init) {
+      CK(cudaFuncSetAttribute(cta_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTA_SMEM_MAX));
+      for (int k = 0; k < 3; k++) {
+        CK(cudaStreamCreateWithFlags(&cls_st[k], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&join_ev[k], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+      init = true;
+    }
+    auto cls_of = [&](u32 i, u64 *need) -> int {
       u64 s = cta_smem_need(h_dims[3 * i], h_dims[3 * i + 1], h_dims[3 * i + 2]);
-      if (s <= CTA_SMEM_MAX && s > smem) smem = s;
-    }
-    smem = (smem + 15) & ~15ull;
-    static u64 attr_set = 0;
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(cta_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTA_SMEM_MAX);
-      if (getenv("DTR_DEBUG")) fprintf(stderr, "dtr: smem=%llu set_attr=%s\n", smem, cudaGetErrorString(e));
-      if (e != cudaSuccess) return cuda_fail(e);
-      attr_set = CTA_SMEM_MAX;
-    }
-    if (getenv("DTR_DEBUG")) fprintf(stderr, "dtr: launch cta n_cells=%u smem=%llu\n", n_cells, smem);
-    cta_engine<<<n_cells, CTA_THREADS, smem, st>>>(d_words, d_cells, n_cells, ws, ws_bytes, d_rows, d_trace,
+      *need = s;
+      return s <= 48 * 1024 - 1024 ? 0 : (s <= CTA_SMEM_MAX ? 1 : 2);
+    };
+    bool used[3] = {false, false, false};
+    u64 first_need;
+    const int c_first = cls_of(0, &first_need);
+    bool single = true;
+    for (u32 i = 1; i < n_cells && single; i++) { u64 nd; single = cls_of(i, &nd) == c_first; }
+    if (!single) CK(cudaEventRecord(fork_ev, st));
+    u32 i = 0;
+    while (i < n_cells) {
+      u64 need;
+      const int c = cls_of(i, &need);
+      u64 smem = c == 2 ? 0 : need;
+      u32 j = i + 1;
+      for (; j < n_cells; j++) {
+        u64 nd;
+        if (cls_of(j, &nd) != c) break;
+        if (c != 2 && nd > smem) smem = nd;
+      }
+      smem = (smem + 15) & ~15ull;
+      cudaStream_t ls = st;
+      if (!single) {
+        ls = cls_st[c];
+        if (!used[c]) { CK(cudaStreamWaitEvent(ls, fork_ev, 0)); used[c] = true; }
+      }
+      if (getenv("DTR_DEBUG")) fprintf(stderr, "dtr: cta launch cells [%u,%u) class %d smem %llu\n", i, j, c, smem);
+      cta_engine<<<j - i, CTA_THREADS, smem, ls>>>(d_words, d_cells, i, j - i, ws, ws_bytes, d_rows, d_trace,
                                                    (u32)smem);
-    CK(cudaGetLastError());
+      CK(cudaGetLastError());
+      i = j;
+    }
+    if (!single) {
+      for (int k = 0; k < 3; k++) {
+        if (!used[k]) continue;
+        CK(cudaEventRecord(join_ev[k], cls_st[k]));
+        CK(cudaStreamWaitEvent(st, join_ev[k], 0));
+      }
+    }
   } else {
     int blocks;
     rc = grid_blocks(&blocks);

@@ -1,0 +1,133 @@
+"""Budget x heuristic sweeps sharded over GPUs.
+
+The paper's methodology (Fig. 2): every (op log, budget
+ratio, heuristic) cell is an independent simulation.  Cells are assigned to
+ranks by a deterministic longest-processing-time-first greedy on an estimated
+cost; each rank replays its cells with the CUDA engines (one launch per
+shared-memory class, CTA per simulation; logs too large for a CTA go to the
+whole-GPU engine); then ONE collective -- all_gather_into_tensor of fixed-size
+result tables over NCCL (NVLink 5 / NVSwitch) -- gives every rank the full
+table, reordered by cell id.  There is no per-decision communication: a single
+simulation does not shard.
+
+Host logic only (argument marshalling and bookkeeping); every replay runs in
+libdtr.so kernels.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .binding import (DeviceBatch, RESULT_DTYPE, ENGINE_CTA, ENGINE_GRID, HEURISTICS)
+
+# relative per-decision cost of a heuristic's score (MSPS walks closures)
+HEUR_WEIGHT = {0: 3.0, 1: 3.0, 2: 1.0, 3: 1.0, 4: 6.0, 5: 1.5, 6: 1.0}
+GRID_MIN_TENSORS = 65536   # logs at least this large replay on the whole-GPU engine
+
+
+def make_cells(log_views, permilles, heuristics, thrash_kill=16, max_decisions=0):
+    """Cells of a sweep: every log x budget permille x heuristic (names or ids).
+    Returns a list of dicts {cell_id, log, permille, budget, heuristic, ...}."""
+    cells = []
+    for li, v in enumerate(log_views):
+        for h in heuristics:
+            hid = HEURISTICS[h] if isinstance(h, str) else int(h)
+            for pm in permilles:
+                cells.append(dict(cell_id=len(cells), log=li, permille=int(pm), budget=v.budget(pm),
+                                  heuristic=hid, thrash_kill=thrash_kill, max_decisions=max_decisions))
+    return cells
+
+
+def est_cost(cell, log_views):
+    v = log_views[cell["log"]]
+    pm = max(int(cell.get("permille", 1000)), 50)
+    return v.n_ops * (1000.0 / pm) * HEUR_WEIGHT.get(cell["heuristic"], 1.0)
+
+
+def shard(cells, log_views, world_size):
+    """Deterministic LPT: sort by estimated cost (desc, then cell id), give each
+    cell to the least-loaded rank (ties -> lowest rank). Returns per-rank lists."""
+    order = sorted(cells, key=lambda c: (-est_cost(c, log_views), c["cell_id"]))
+    load = [0.0] * world_size
+    out = [[] for _ in range(world_size)]
+    for c in order:
+        r = min(range(world_size), key=lambda k: (load[k], k))
+        out[r].append(c)
+        load[r] += est_cost(c, log_views)
+    for r in range(world_size):
+        out[r].sort(key=lambda c: c["cell_id"])
+    return out
+
+
+def engine_groups(cells, log_views):
+    """Split a rank's cells into the CTA-engine group and the grid-engine group."""
+    cta = [c for c in cells if log_views[c["log"]].n < GRID_MIN_TENSORS]
+    grid = [c for c in cells if log_views[c["log"]].n >= GRID_MIN_TENSORS]
+    return cta, grid
+
+
+class RankSweep:
+    """The device side of one rank: its cells as (up to) two resident batches."""
+
+    def __init__(self, logs, log_views, cells, device=None):
+        self.cells = cells
+        cta, grid = engine_groups(cells, log_views)
+        # order CTA cells by log so shared-memory classes form few launches
+        cta.sort(key=lambda c: (log_views[c["log"]].n, c["log"], c["cell_id"]))
+        self.order = cta + grid
+        self.batches = []
+        for group, eng in ((cta, ENGINE_CTA), (grid, ENGINE_GRID)):
+            if group:
+                self.batches.append(DeviceBatch(logs, group, engine=eng, device=device))
+
+    def run(self, stream=None):
+        for b in self.batches:
+            b.run(stream)
+
+    def rows_device(self):
+        import torch
+        return torch.cat([b.rows for b in self.batches]) if self.batches else None
+
+
+def gather_rows(local_rows_u8, n_local, max_local, world_size, group=None):
+    """all_gather_into_tensor of fixed-size row tables (padded to max_local rows);
+    returns the concatenated table as a numpy structured array (valid rows only)."""
+    import torch
+    import torch.distributed as dist
+    rb = RESULT_DTYPE.itemsize
+    dev = local_rows_u8.device
+    padded = torch.zeros(max_local * rb, dtype=torch.uint8, device=dev)
+    if n_local:
+        padded[: n_local * rb] = local_rows_u8[: n_local * rb]
+    counts = torch.tensor([n_local], dtype=torch.int64, device=dev)
+    all_counts = torch.zeros(world_size, dtype=torch.int64, device=dev)
+    out = torch.zeros(world_size * max_local * rb, dtype=torch.uint8, device=dev)
+    if world_size > 1:
+        dist.all_gather_into_tensor(all_counts, counts, group=group)
+        dist.all_gather_into_tensor(out, padded, group=group)
+    else:
+        all_counts.copy_(counts)
+        out.copy_(padded)
+    table = out.cpu().numpy().view(RESULT_DTYPE).reshape(world_size, max_local)
+    cnt = all_counts.cpu().numpy()
+    return np.concatenate([table[r, : int(cnt[r])] for r in range(world_size)])
+
+
+def order_by_cell(rows):
+    return rows[np.argsort(rows["cell_id"], kind="stable")]
+
+
+def run_sweep(logs, log_views, cells, rank=0, world_size=1, device=None, group=None):
+    """Replay every cell of a sweep across the process group; every rank returns
+    the full table ordered by cell id."""
+    import torch
+    shards = shard(cells, log_views, world_size)
+    mine = shards[rank]
+    rs = RankSweep(logs, log_views, mine, device=device)
+    rs.run()
+    torch.cuda.synchronize()
+    local = rs.rows_device()
+    if local is None:
+        local = torch.zeros(0, dtype=torch.uint8, device=device or "cuda")
+    max_local = max(len(s) for s in shards)
+    rows = gather_rows(local, len(mine), max(max_local, 1), world_size, group)
+    return order_by_cell(rows)
