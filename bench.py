@@ -219,6 +219,7 @@ def main():
     batch = P.DeviceBatch(logs, specs, engine=P.ENGINE_CTA)
     stream = torch.cuda.current_stream(dev)
     n_cells = len(specs)
+    launches_per_step = 1          # one cta_engine launch (all 120 cells share one shared-memory class)
     rows_all = torch.empty(ws * batch.rows.numel(), dtype=torch.uint8, device=dev) if ws > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -330,7 +331,7 @@ def main():
            "e2e": {"value": e2e_value, "unit": "decisions/s",
                    "h2d_bytes_per_step": int(words.nbytes + cells.nbytes + 12 * n_cells),
                    "d2h_bytes_per_step": int(n_cells * P.RESULT_DTYPE.itemsize)},
-           "gpu_launches": 2 * args.steps,
+           "gpu_launches": launches_per_step * args.steps,
            "roofline": roof,
            "clocks": clocks,
            "wall_s_timed": wall}
