@@ -4,7 +4,7 @@
 Workload (BASELINE.json configs[1], "config2"): the ResNet-32-shaped synthetic op
 log, budget ratios 0.1..1.0 (30 permilles) x {h_DTR, h_DTR_eq, LRU, size} = 120
 independent simulations per GPU (weak scaling: rank r replays its own log drawn
-with seed r).  One step = one dtr_replay_batch over those 120 cells (plan kernel +
+with seed r).  One step = one dtr_replay_batch over those 120 cells (
 one CTA-per-simulation engine launch) [+ one NCCL all_gather of the result rows
 when N > 1].
 
@@ -16,9 +16,9 @@ when N > 1].
   roofline: the CTA engine (dominant kernel): algorithmic score-pass bytes per
             launch (sum of rows' score_bytes) / its average
             CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
-  roofline_large_pool: the grid engine on the config-5s stress log (1e6-tensor
-            random locality DAG, pool ~1e6): per-decision bytes / per-decision time,
-            isolated as the difference of two decision caps.
+  roofline_large_pool: K3+K4 alone (dtr_pool_argmin: score pass + exact argmin)
+            over the ~1e6-tensor pool of the config-5s stress log after 1000 grid-engine
+            decisions; algorithmic bytes per launch / CUDA-event launch time.
   cpu_baseline: the CPU oracle (oracle/, plain C, unmodified) on the host cores,
             process pool, bounded sample of the same cells (rank 0, N = 1 only).
 
@@ -350,37 +350,40 @@ def main():
         dist.destroy_process_group()
 
 
-def large_pool(P, torch, dev, n, hbm_peak, peak_src):
-    """Grid engine on the config-5s stress log: per-decision score+argmin cost at a ~n pool."""
+def large_pool(P, torch, dev, n, hbm_peak, peak_src, D=1000, reps=20):
+    """K3+K4 alone at a ~n pool: replay the config-5s stress log on the grid engine
+    up to its D-th eviction decision (h_DTR), then time dtr_pool_argmin -- the
+    score pass + exact argmin over the resident pool -- with CUDA events, L2
+    flushed (256 MiB write) before every launch."""
     w = models.random_dag(n, seed=0)
     v = LogView(w)
-    res = {}
-    for D in (32, 160):
-        spec = [dict(log=0, budget=v.peak_total * 98 // 100, heuristic=0, thrash_kill=16, max_decisions=D)]
-        b = P.DeviceBatch([w], spec, engine=P.ENGINE_GRID)
-        s = torch.cuda.current_stream(dev)
-        b.run(s)
+    spec = [dict(log=0, budget=v.peak_total * 98 // 100, heuristic=0, thrash_kill=16, max_decisions=D)]
+    b = P.DeviceBatch([w], spec, engine=P.ENGINE_GRID)
+    s = torch.cuda.current_stream(dev)
+    b.run(s)
+    torch.cuda.synchronize()
+    row = b.result_rows()[0]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        b.pool_argmin(stream=s)
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        out = b.pool_argmin(stream=s)
+        e1.record(s)
         torch.cuda.synchronize()
-        ts = []
-        for _ in range(3):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
-            b.run(s)
-            e1.record(s)
-            torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1) / 1e3)
-        r = b.result_rows()[0]
-        res[D] = (min(ts), int(r["score_bytes"]), int(r["cand_evals"]), int(r["decisions"]))
-        del b
-    (t0, b0, c0, d0), (t1, b1, c1, d1) = res[32], res[160]
-    dt = (t1 - t0) / (d1 - d0)
-    bpd = (b1 - b0) / (d1 - d0)
-    ach = bpd / dt / 1e9
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    o = out.cpu().numpy()
+    t = sum(ts) / len(ts)
+    ach = float(o[3]) / t / 1e9
     return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-            "traffic": None, "peak_source": peak_src, "kernel": "grid_engine (h_DTR)",
-            "workload": f"config5s random locality DAG n={n}, B=0.98*peak_total",
-            "pool_per_decision": (c1 - c0) / (d1 - d0), "bytes_per_decision": bpd, "us_per_decision": dt * 1e6,
-            "decisions_per_s": 1.0 / dt}
+            "traffic": None, "peak_source": peak_src, "kernel": "pool_argmin_kernel (K3+K4, h_DTR)",
+            "workload": f"config5s random locality DAG n={n}, B=0.98*peak_total, pool after {int(row['decisions'])} "
+                        f"decisions", "pool": int(o[4]), "bytes_per_launch": int(o[3]),
+            "us_per_launch": t * 1e6, "launches": reps, "l2": "flushed before every launch",
+            "decisions_per_s_score_only": 1.0 / t}
 
 
 if __name__ == "__main__":

@@ -145,6 +145,15 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
                      uint32_t n_cells, uint32_t engine, void *d_ws, uint64_t ws_bytes,
                      dtr_result *d_rows, dtr_evict_rec *d_trace, void *stream);
 
+/* K3+K4 alone (score pass + exact argmin) over the current pool of the
+ * simulation left in a grid-engine workspace by the last dtr_replay_batch
+ * (DTR_ENGINE_GRID) call -- e.g. one stopped with DTR_E_DECISION_CAP: "which
+ * tensor would free() evict next".  d_log: device pointer to that cell's log
+ * (words + log_offset).  heuristic: the cell's.  d_out: device, 5 uint64
+ * {num, den, id, score_bytes, cand_evals}; id = 0xFFFFFFFF for an empty pool.
+ * Asynchronous on `stream`; does not modify the simulation. */
+int dtr_pool_argmin(const uint32_t *d_log, uint32_t heuristic, void *d_ws, uint64_t *d_out, void *stream);
+
 /* End-to-end convenience: host inputs and outputs.  Copies h_words (n_words)
  * and h_cells to the device, replays (engine as above; 0 = choose per size),
  * copies rows (and trace_total trace records when h_trace != NULL) back, and

@@ -37,7 +37,7 @@ assert TRACE_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 88 and CELL_DTYPE
 EXPORTS = ["dtr_strerror", "dtr_last_cuda_error", "dtr_version", "dtr_batch_workspace_bytes",
            "dtr_replay_batch", "dtr_replay_batch_host", "dtr_create", "dtr_destroy", "dtr_compute", "dtr_get",
            "dtr_release", "dtr_rematerialize", "dtr_ensure", "dtr_stats", "dtr_trace", "dtr_debug_evict",
-           "dtr_debug_set_budget", "dtr_debug_scores"]
+           "dtr_debug_set_budget", "dtr_debug_scores", "dtr_pool_argmin"]
 
 
 class DtrError(RuntimeError):
@@ -67,6 +67,8 @@ def _load():
     L.dtr_batch_workspace_bytes.argtypes = [P, u32, u32, C.POINTER(u64)]
     L.dtr_replay_batch.restype = i32
     L.dtr_replay_batch.argtypes = [P, P, P, u32, u32, P, u64, P, P, P]
+    L.dtr_pool_argmin.restype = i32
+    L.dtr_pool_argmin.argtypes = [P, u32, P, P, P]
     L.dtr_replay_batch_host.restype = i32
     L.dtr_replay_batch_host.argtypes = [P, u64, P, u32, u32, P, P, u64, P]
     L.dtr_create.restype = i32
@@ -203,6 +205,19 @@ class DeviceBatch:
         replay_batch(self.words.data_ptr(), self.cells.data_ptr(), self.h_dims, self.n_cells, self.engine,
                      self.ws.data_ptr(), self.ws_bytes, self.rows.data_ptr(),
                      self.trace.data_ptr() if self.trace is not None else None, s.cuda_stream)
+
+    def pool_argmin(self, cell=0, stream=None):
+        """dtr_pool_argmin over the grid-engine workspace (call after run()).
+        Returns (num, den, id, score_bytes, cand_evals) as a device tensor of 5 int64."""
+        torch = self.torch
+        assert self.engine == ENGINE_GRID
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_pa_out"):
+            self._pa_out = torch.zeros(5, dtype=torch.int64, device=self.device)
+        log_ptr = self.words.data_ptr() + 4 * int(self.h_cells[cell]["log_offset"])
+        _check(lib.dtr_pool_argmin(log_ptr, int(self.h_cells[cell]["heuristic"]), self.ws.data_ptr(),
+                                   self._pa_out.data_ptr(), s.cuda_stream), "dtr_pool_argmin")
+        return self._pa_out
 
     def result_rows(self):
         return self.rows.cpu().numpy().view(RESULT_DTYPE).copy()

@@ -32,7 +32,10 @@ using namespace dtr;
 #define CTA_THREADS 256
 #define GRID_THREADS 512
 #define GRID_MSPS_WARPS 1024
-#define WS_HEADER 98560ull   /* 256 + 4096 * sizeof(Cand), multiple of 256 */
+#define WS_HEADER 164352ull  /* 512 + 4096 * (sizeof(Cand) + 16), multiple of 256 */
+#define WS_BSTATS 98816      /* per-block {bytes, evals} for dtr_pool_argmin */
+#define WS_SCALARS 128       /* grid engine: final Scalars of the last cell */
+#define WS_PARTIALS 512
 #define CTA_SMEM_MAX (200u * 1024u)
 
 // ---------------------------------------------------------------------------
@@ -84,14 +87,15 @@ __device__ void init_sim(const Sim<SM> &g, const u32 *logw, u32 rank, u32 size, 
   for (u32 t = rank; t < n; t += size) {
     const u32 b = loff[t], e = loff[t + 1];
     g.srec(t) = make_uint4(lmem[t], lcost[t], b, e - b);
-    g.drec(t) = make_uint4(0, 0, 0, 0);
-    g.crec(t) = make_uint2(0, 0);
+    g.state(t) = 0; g.la(t) = 0; g.rho(t) = 0; g.ell(t) = 0;
     g.pool_pos(t) = NONE;
+    g.crec(t) = make_uint2(0, 0);
     g.m.w(g.L.fr + t) = 0;                      // fill cursor (the stack is unused until the leader starts)
     if (heur == H_DTR) g.m.w(g.L.stamp + t) = 0;
     if (heur == H_DTR_EQ) g.m.w(g.L.node_of + t) = NONE;
   }
   for (u32 j = rank; j < E; j += size) g.par(j) = lpar[j];
+  for (u32 w = rank; w < g.L.pool_words; w += size) g.pool_word(w) = 0;
   if (heur == H_MSPS) {
     const u32 words = g.L.msps_words * g.L.msps_warps;
     for (u32 i = rank; i < words; i += size) g.m.w(g.L.msps_bm + i) = 0;
@@ -160,11 +164,11 @@ __device__ void write_row(dtr_result &r, const Scalars &s, u64 bytes, u64 evals)
 
 __device__ __forceinline__ void publish(Cmd &c, u32 kind, const Scalars &s) {
   c.kind = kind; c.pool_size = s.pool_size; c.clock = s.clock; c.decisions = s.decisions;
-  c.seed = s.seed; c.heur = s.heuristic; c.pad = 0;
+  c.seed = s.seed; c.heur = s.heuristic; c.n_ids = s.n_alloc;
 }
 
-template <bool SM>
-__device__ __forceinline__ void leader_init(Leader<SM> &L, const Sim<SM> &g, const u32 *logw, const dtr_cell &cell,
+template <bool SM, bool BM>
+__device__ __forceinline__ void leader_init(Leader<SM, BM> &L, const Sim<SM> &g, const u32 *logw, const dtr_cell &cell,
                                             dtr_evict_rec *trace) {
   L.g = g;
   init_scalars(L.s, cell);
@@ -219,7 +223,7 @@ __device__ __forceinline__ Cmd shfl_cmd(const Cmd &c) {
   r.decisions = __shfl_sync(0xffffffffu, c.decisions, 0);
   r.seed = __shfl_sync(0xffffffffu, c.seed, 0);
   r.heur = __shfl_sync(0xffffffffu, c.heur, 0);
-  r.pad = 0;
+  r.n_ids = __shfl_sync(0xffffffffu, c.n_ids, 0);
   return r;
 }
 
@@ -247,7 +251,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   if (tid == 0) PROF_ADD(6, ti1 - ti0);
   u64 bytes = 0, evals = 0;
   if (warp == 0) {
-    Leader<SM> L;
+    Leader<SM, false> L;
     if (lane == 0) leader_init(L, g, logw, cell, trace);
     Cand res = cand_none();
     bool have = false;
@@ -265,7 +269,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       if (c.kind == CMD_ARGMIN && c.pool_size <= WARP_TEAM_MAX) {
         PROF_T(t2);
         u32 bk;
-        Cand best = team_score(g, c, lane, 32, 0, 1, sh.msps_tail, bytes, evals, bk);
+        Cand best = team_score<SM, false>(g, c, lane, 32, 0, 1, sh.msps_tail, bytes, evals, bk);
         PROF_T(t3);
         best = warp_argmin_fast(best, bk);
         PROF_T(t4);
@@ -277,7 +281,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       __syncthreads();
       if (c.kind != CMD_ARGMIN) break;
       u32 bk;
-      Cand best = team_score(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk);
+      Cand best = team_score<SM, false>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk);
       best = block_argmin(best, bk, sh.red);
       PROF_T(t6);
       if (lane == 0) { res = best; have = true; PROF_ADD(4, t6 - t5); PROF_ADD(5, 1); }
@@ -289,7 +293,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       const Cmd c = sh.cmd;
       if (c.kind != CMD_ARGMIN) break;
       u32 bk;
-      Cand best = team_score(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk);
+      Cand best = team_score<SM, false>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk);
       block_argmin(best, bk, sh.red);
     }
   }
@@ -297,7 +301,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   if (tid == 0) { row->score_bytes = bytes; row->cand_evals = evals; }
 }
 
-__global__ void __launch_bounds__(CTA_THREADS) cta_engine(const u32 *words, const dtr_cell *cells, u32 c0, u32 n_run,
+__global__ void __launch_bounds__(CTA_THREADS, 1) cta_engine(const u32 *words, const dtr_cell *cells, u32 c0, u32 n_run,
                                                           char *ws, u64 ws_bytes, dtr_result *rows,
                                                           dtr_evict_rec *trace, u32 smem_bytes) {
   __shared__ CtaShared sh;
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
   const u32 tid = threadIdx.x;
   Cmd *gcmd = (Cmd *)ws;
   u64 *gstats = (u64 *)(ws + 64);   // [bytes, evals]
-  Cand *partials = (Cand *)(ws + 256);
+  Cand *partials = (Cand *)(ws + WS_PARTIALS);
   const dtr_cell cell = cells[ci];
   const u32 *logw = words + cell.log_offset;
   if (WS_HEADER + cell_bytes(logw[2], logw[3], cell.heuristic, DTR_ENGINE_GRID) > ws_bytes) {
@@ -370,9 +374,9 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
   make_layout(g.L, logw[2], logw[3], cell.heuristic, 0, GRID_MSPS_WARPS);
   const u32 rank = blockIdx.x * blockDim.x + tid, size = gridDim.x * blockDim.x;
   const u32 wrank = rank >> 5, wsize = size >> 5;
-  if (rank == 0) { gstats[0] = 0; gstats[1] = 0; }
+  if (rank == 0) { gstats[0] = 0; gstats[1] = 0; *(u32 *)(ws + 120) = 0; }
   init_sim(g, logw, rank, size, blockIdx.x == 0, sh.scan, GridSync());
-  Leader<false> L;
+  Leader<false, true> L;
   if (rank == 0) leader_init(L, g, logw, cell, trace);
   Cand res = cand_none();
   bool have = false;
@@ -397,13 +401,14 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
       Cmd c;
       c.kind = __ldcg(&gcmd->kind); c.pool_size = __ldcg(&gcmd->pool_size); c.clock = __ldcg(&gcmd->clock);
       c.decisions = __ldcg(&gcmd->decisions); c.seed = __ldcg(&gcmd->seed); c.heur = __ldcg(&gcmd->heur);
+      c.n_ids = __ldcg(&gcmd->n_ids);
       sh.cmd = c;
     }
     __syncthreads();
     if (sh.cmd.kind != CMD_ARGMIN) break;
     u32 bk;
     PROF_T(c0);
-    Cand best = team_score(g, sh.cmd, rank, size, wrank, wsize, sh.msps_tail, bytes, evals, bk);
+    Cand best = team_score<false, true, true>(g, sh.cmd, rank, size, wrank, wsize, sh.msps_tail, bytes, evals, bk);
     PROF_T(c1);
     best = block_argmin(best, bk, sh.red);
     if (tid == 0) partials[blockIdx.x] = best;
@@ -428,7 +433,69 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
   block_sum2(bytes, evals, sh.red);
   if (tid == 0) { atomicAdd(&gstats[0], bytes); atomicAdd(&gstats[1], evals); }
   grid.sync();
-  if (rank == 0) write_row(rows[ci], L.s, __ldcg(&gstats[0]), __ldcg(&gstats[1]));
+  if (rank == 0) {
+    write_row(rows[ci], L.s, __ldcg(&gstats[0]), __ldcg(&gstats[1]));
+    *(Scalars *)(ws + WS_SCALARS) = L.s;   // kept for dtr_pool_argmin
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3+K4 alone: score the current pool of the simulation left in a grid-engine
+// workspace and reduce its argmin (last-block reduction, no cooperative sync).
+// Used to time the score pass in isolation (bench roofline_large_pool).
+// ---------------------------------------------------------------------------
+#define PA_THREADS 256
+struct __align__(16) PaShared {
+  RedSmem red;
+  u32 msps_tail[PA_THREADS / 32];
+};
+
+__global__ void __launch_bounds__(PA_THREADS, 3) pool_argmin_kernel(const u32 *logw, u32 heur, char *ws,
+                                                                    u64 *out /* num, den, id, bytes, evals */) {
+  __shared__ PaShared sh;
+  __shared__ bool last;
+  const u32 tid = threadIdx.x;
+  Cand *partials = (Cand *)(ws + WS_PARTIALS);
+  u32 *arrive = (u32 *)(ws + 120);
+  Sim<false> g;
+  g.m.gbase = (u32 *)(ws + WS_HEADER);
+  make_layout(g.L, logw[2], logw[3], heur, 0, GRID_MSPS_WARPS);
+  const Scalars *sc = (const Scalars *)(ws + WS_SCALARS);
+  Cmd cmd;
+  cmd.kind = CMD_ARGMIN; cmd.pool_size = sc->pool_size; cmd.clock = sc->clock; cmd.decisions = sc->decisions;
+  cmd.seed = sc->seed; cmd.heur = heur; cmd.n_ids = sc->n_alloc;
+  const u32 rank = blockIdx.x * blockDim.x + tid, size = gridDim.x * blockDim.x;
+  u64 bytes = 0, evals = 0;
+  u32 bk;
+  Cand best = team_score<false, true, true>(g, cmd, rank, size, rank >> 5, size >> 5, sh.msps_tail, bytes, evals, bk);
+  best = block_argmin(best, bk, sh.red);
+  block_sum2(bytes, evals, sh.red);
+  u64 *bstats = (u64 *)(ws + WS_BSTATS);
+  if (tid == 0) {
+    partials[blockIdx.x] = best;
+    bstats[2 * blockIdx.x] = bytes;
+    bstats[2 * blockIdx.x + 1] = evals;
+    __threadfence();
+    last = atomicAdd(arrive, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && tid < 32) {
+    __threadfence();
+    Cand c = cand_none();
+    u32 ck = KEY_NONE;
+    u64 tb = 0, te = 0;
+    for (u32 b = tid; b < gridDim.x; b += 32) {
+      Cand d;
+      d.num = __ldcg(&partials[b].num); d.den = __ldcg(&partials[b].den); d.id = __ldcg(&partials[b].id);
+      cand_take(c, ck, d);
+      tb += __ldcg(&bstats[2 * b]);
+      te += __ldcg(&bstats[2 * b + 1]);
+    }
+    c = warp_argmin_fast(c, ck);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { tb += __shfl_xor_sync(0xffffffffu, tb, o); te += __shfl_xor_sync(0xffffffffu, te, o); }
+    if (tid == 0) { out[0] = c.num; out[1] = c.den; out[2] = c.id; out[3] = tb; out[4] = te; *arrive = 0; }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -453,10 +520,11 @@ __global__ void __launch_bounds__(CTA_THREADS) percall_engine(PercallArgs a) {
   g.m.gbase = a.base;
   g.L = a.L;
   if (a.init) {
+    for (u32 w = tid; w < g.L.pool_words; w += blockDim.x) g.pool_word(w) = 0;
     for (u32 t = tid; t <= g.L.n; t += blockDim.x) {
-      g.drec(t) = make_uint4(0, 0, 0, 0);
-      g.crec(t) = make_uint2(NONE, 0);
+      g.state(t) = 0; g.la(t) = 0; g.rho(t) = 0; g.ell(t) = 0;
       g.pool_pos(t) = NONE;
+      g.crec(t) = make_uint2(NONE, 0);
       if (g.L.heur == H_DTR) g.m.w(g.L.stamp + t) = 0;
       if (g.L.heur == H_DTR_EQ) g.m.w(g.L.node_of + t) = NONE;
     }
@@ -466,7 +534,7 @@ __global__ void __launch_bounds__(CTA_THREADS) percall_engine(PercallArgs a) {
     }
     return;
   }
-  Leader<false> L;
+  Leader<false, false> L;
   if (tid == 0) {
     L.g = g;
     L.s = *a.sc;
@@ -494,7 +562,8 @@ __global__ void __launch_bounds__(CTA_THREADS) percall_engine(PercallArgs a) {
     }
     u64 junk = 0, junk2 = 0;
     u32 bk;
-    Cand best = team_score(g, sh.cmd, tid, blockDim.x, tid >> 5, blockDim.x >> 5, sh.msps_tail, junk, junk2, bk);
+    Cand best = team_score<false, false>(g, sh.cmd, tid, blockDim.x, tid >> 5, blockDim.x >> 5, sh.msps_tail, junk, junk2,
+                                         bk);
     best = block_argmin(best, bk, sh.red);
     if (tid == 0) { res = best; have = true; }
   }
@@ -649,6 +718,20 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
       CK(cudaLaunchCooperativeKernel((void *)grid_engine, dim3(blocks), dim3(GRID_THREADS), args, 0, st));
     }
   }
+  return DTR_OK;
+}
+
+int dtr_pool_argmin(const uint32_t *d_log, uint32_t heuristic, void *d_ws, uint64_t *d_out, void *stream) {
+  if (!d_log || !d_ws || !d_out || heuristic > H_RANDOM) return DTR_E_INVAL;
+  int dev, sms, per_sm = 0, blocks;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pool_argmin_kernel, PA_THREADS, 0));
+  blocks = sms * (per_sm < 1 ? 1 : per_sm);
+  if (blocks > 4096) blocks = 4096;
+  cudaStream_t st = (cudaStream_t)stream;
+  pool_argmin_kernel<<<blocks, PA_THREADS, 0, st>>>(d_log, heuristic, (char *)d_ws, (u64 *)d_out);
+  CK(cudaGetLastError());
   return DTR_OK;
 }
 

@@ -11,11 +11,17 @@
 //
 // Memory: every array of a simulation is addressed by a 32-bit WORD offset from
 // one base -- the CTA's dynamic shared memory (SM = true: LDS/STS, 32-bit
-// addresses) or the simulation's global workspace (SM = false).  Per-tensor
-// data is array-of-structs so the leader fetches a tensor with one 16-B load:
-//   srec[t] = {mem, cost, par_off, npar}          (static, from the log)
+// addresses) or the simulation's global workspace (SM = false).
+//   srec[t] = {mem, cost, par_off, npar}          (static, from the log; one 16-B load)
 //   crec[t] = {ch_off, nch}  | linked: {head, -}  (children, built on device)
-//   drec[t] = {state, la, rho, ell}               (dynamic)
+//   state[t], la[t], rho[t], ell[t]               (dynamic, compact u32 arrays: a
+//             neighbour's state word shares its sector with nearby ids)
+//   pool     R.pool (t.m = T and t.l = 0), one of two representations:
+//            - compact list pool_ids[] + pool_pos[] (CTA engine, per-call): the
+//              team scans exactly the P members;
+//            - bitmap over tensor ids (whole-GPU engine): the team scans ids in
+//              order, so a warp's candidates are consecutive ids whose (mostly
+//              nearby) neighbours share sectors and L1 lines
 //   state: bit31 material (t.m = T), bit30 computed once (reading C-19),
 //          bits 0..29 label of t's evicted component (h_DTR)
 //   la:    last_access + 1, 0 = -inf (banish_V2)
@@ -51,7 +57,7 @@ __host__ __device__ __forceinline__ bool is_material(u32 s) { return (s & M_BIT)
 // ---------------------------------------------------------------------------
 struct Lay {
   u32 n, E, heur, linked;
-  u32 srec, crec, par, ch, drec, pool_ids, pool_pos, fr, pb;
+  u32 srec, crec, par, ch, state, la, rho, ell, pool_bm, pool_words, pool_ids, pool_pos, fr, pb;
   u32 mem_next, comp, comp_head, bfs_q, stamp;         // h_DTR (comp rec: {cost lo, cost hi, maxla, size})
   u32 node_of, uf, uf_size, uf_cap;                    // h_DTR_eq (uf rec: {cost lo, cost hi, maxla, parent})
   u32 msps_bm, msps_q, msps_words, msps_warps;         // h_MSPS per-warp scratch
@@ -71,7 +77,12 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
   L.crec = take(2 * n1);
   L.par = take(e1);
   L.ch = linked ? 0 : take(e1);
-  L.drec = take(4 * n1);
+  L.state = take(n1);
+  L.la = take(n1);
+  L.rho = take(n1);
+  L.ell = take(n1);
+  L.pool_words = (u32)((n1 + 31) / 32);
+  L.pool_bm = take(L.pool_words);
   L.pool_ids = take(n1);
   L.pool_pos = take(n1);
   L.fr = take(4 * n1);
@@ -217,12 +228,13 @@ struct Sim {
 
   __device__ __forceinline__ uint4 &srec(u32 t) const { return m.q(L.srec + 4 * t); }
   __device__ __forceinline__ uint2 &crec(u32 t) const { return m.d(L.crec + 2 * t); }
-  __device__ __forceinline__ uint4 &drec(u32 t) const { return m.q(L.drec + 4 * t); }
-  __device__ __forceinline__ u32 &state(u32 t) const { return m.w(L.drec + 4 * t); }
-  __device__ __forceinline__ u32 &la(u32 t) const { return m.w(L.drec + 4 * t + 1); }
-  __device__ __forceinline__ u32 &rho(u32 t) const { return m.w(L.drec + 4 * t + 2); }
-  __device__ __forceinline__ u32 &ell(u32 t) const { return m.w(L.drec + 4 * t + 3); }
+  __device__ __forceinline__ u32 &state(u32 t) const { return m.w(L.state + t); }
+  __device__ __forceinline__ u32 &la(u32 t) const { return m.w(L.la + t); }
+  __device__ __forceinline__ u32 &rho(u32 t) const { return m.w(L.rho + t); }
+  __device__ __forceinline__ u32 &ell(u32 t) const { return m.w(L.ell + t); }
   __device__ __forceinline__ u32 &par(u32 j) const { return m.w(L.par + j); }
+  __device__ __forceinline__ u32 &pool_word(u32 w) const { return m.w(L.pool_bm + w); }
+  __device__ __forceinline__ bool in_pool(u32 t) const { return (pool_word(t >> 5) >> (t & 31)) & 1u; }
   __device__ __forceinline__ u32 &pool_ids(u32 i) const { return m.w(L.pool_ids + i); }
   __device__ __forceinline__ u32 &pool_pos(u32 t) const { return m.w(L.pool_pos + t); }
   __device__ __forceinline__ uint4 &comp(u32 c) const { return m.q(L.comp + 4 * c); }

@@ -27,10 +27,10 @@ enum { CMD_DONE = 0, CMD_ARGMIN = 1, CMD_SCORES = 2 };
 
 struct Cmd {
   u64 clock, decisions, seed;
-  u32 kind, pool_size, heur, pad;
+  u32 kind, pool_size, heur, n_ids;   // n_ids: tensor ids [0, n_ids) to scan for pool members
 };
 
-template <bool SM>
+template <bool SM, bool BM>
 struct Leader {
   Sim<SM> g;
   Scalars s;
@@ -42,18 +42,35 @@ struct Leader {
   u64 free_size;
 
   // ------------------------------------------------------------- pool
+  // R.pool: bitmap over tensor ids (BM) or compact list with positions
   __device__ __forceinline__ void pool_add(u32 t) {
-    u32 k = s.pool_size++;
-    g.pool_pos(t) = k;
-    g.pool_ids(k) = t;
+    if constexpr (BM) {
+      g.pool_word(t >> 5) |= 1u << (t & 31);
+      s.pool_size++;
+    } else {
+      const u32 k = s.pool_size++;
+      g.pool_pos(t) = k;
+      g.pool_ids(k) = t;
+    }
   }
   __device__ __forceinline__ void pool_remove(u32 t) {
-    u32 p = g.pool_pos(t);
-    if (p == NONE) return;
-    u32 last = g.pool_ids(--s.pool_size);
-    g.pool_ids(p) = last;
-    g.pool_pos(last) = p;
-    g.pool_pos(t) = NONE;
+    if constexpr (BM) {
+      const u32 w = g.pool_word(t >> 5), b = 1u << (t & 31);
+      if (!(w & b)) return;
+      g.pool_word(t >> 5) = w & ~b;
+      s.pool_size--;
+    } else {
+      const u32 p = g.pool_pos(t);
+      if (p == NONE) return;
+      const u32 last = g.pool_ids(--s.pool_size);
+      g.pool_ids(p) = last;
+      g.pool_pos(last) = p;
+      g.pool_pos(t) = NONE;
+    }
+  }
+  __device__ __forceinline__ bool pool_has(u32 t) {
+    if constexpr (BM) return g.in_pool(t);
+    else return g.pool_pos(t) != NONE;
   }
   // get_internal branch "t.m = T": l++, pool \ {t}
   __device__ __forceinline__ void lock(u32 t) {
@@ -375,8 +392,11 @@ struct Leader {
         if (!ok) { if (!precond()) return CMD_DONE; continue; }
         s.base_so_far += sr.y;
         const u32 now = (u32)(s.clock + 1);
-        g.drec(id) = make_uint4(0, now, 1, 0);
-        g.pool_pos(id) = NONE;
+        g.state(id) = 0;
+        g.la(id) = now;
+        g.rho(id) = 1;
+        g.ell(id) = 0;
+        if constexpr (!BM) g.pool_pos(id) = NONE;
         if (s.heuristic == H_DTR_EQ) g.m.w(g.L.node_of + id) = NONE;
         if (g.L.linked) g.crec(id) = make_uint2(NONE, 0);
         for (u32 j = 0; j < sr.w; j++) {          // p.C u= {t}; p.last_accessed := clock
@@ -419,7 +439,7 @@ struct Leader {
         continue;
       }
       if (op == OP_DEBUG_EVICT) {
-        if (id >= s.n_alloc || g.pool_pos(id) == NONE) { if (!precond()) return CMD_DONE; continue; }
+        if (id >= s.n_alloc || !pool_has(id)) { if (!precond()) return CMD_DONE; continue; }
         evict(id);
         finish_op();
         continue;

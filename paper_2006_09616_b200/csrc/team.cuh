@@ -10,10 +10,12 @@
 //   h_MSPS    (c0(t) + sum_{e_R(t)} c0) / m(t)
 //   h_local   c0(t) / (m(t) s(t))
 //   h_random  splitmix64(seed ^ decision << 32 ^ t)                        P:1269 (C-15)
-// Algorithmic bytes per candidate are counted as they are read (DESIGN.md
-// "Roofline"): pool id 4, static record 16, la 4, children record 8, then 8
-// per neighbour (id + state word), 12 per distinct component (cost + max la),
-// h_DTR_eq +4 per evicted neighbour (node id) and +4 per union-find step.
+// Algorithmic bytes are counted as they are read: the
+// pool bitmap (1 bit per tensor id), per candidate its own fields (h_DTR: srec
+// 16 + la 4 + children record 8; LRU la 4; size mem 4; local 12; random 4),
+// then 8 per neighbour (id + state word), 12 per distinct component (cost +
+// max la), h_DTR_eq +4 per evicted neighbour (node id) and +4 per union-find
+// step; MSPS +8 per parent examined, +16 per closure member.
 #pragma once
 #include "engine.cuh"
 #include "leader.cuh"
@@ -60,55 +62,11 @@ __device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const ui
   bytes += 8ull * nb + 12ull * nd + extra;
 }
 
-template <bool SM>
-__device__ __forceinline__ void score_one(const Sim<SM> &g, u32 heur, u64 clock, u64 seed, u64 decisions, u32 t,
-                                          u64 &num, u64 &den, u64 &bytes) {
-  switch (heur) {
-    case H_DTR: {
-      const uint4 sr = g.srec(t);
-      u64 sum = 0;
-      u32 L = g.la(t);
-      nbr_components<SM, false>(g, t, sr, sum, L, bytes);
-      stale_score((u64)sr.y + sum, sr.x, L, clock, num, den);
-      bytes += 4 + 16 + 4 + 8;
-      return;
-    }
-    case H_DTR_EQ: {
-      const uint4 sr = g.srec(t);
-      u64 sum = 0;
-      u32 L = g.la(t);
-      nbr_components<SM, true>(g, t, sr, sum, L, bytes);
-      stale_score((u64)sr.y + sum, sr.x, L, clock, num, den);
-      bytes += 4 + 16 + 4 + 8;
-      return;
-    }
-    case H_LRU:
-      stale_score(1, 1, g.la(t), clock, num, den);
-      bytes += 8;
-      return;
-    case H_SIZE:
-      num = 1; den = g.srec(t).x;
-      bytes += 8;
-      return;
-    case H_LOCAL: {
-      const uint4 sr = g.srec(t);
-      stale_score((u64)sr.y, sr.x, g.la(t), clock, num, den);
-      bytes += 4 + 16 + 4;
-      return;
-    }
-    case H_RANDOM:
-      num = splitmix64(seed ^ (decisions << 32) ^ (u64)t); den = 1;
-      bytes += 4;
-      return;
-  }
-  num = 0; den = 1;
-}
-
 // K5: warp-cooperative e_R(t) -- evicted ancestors reached through evicted
 // parents.  Per-warp visited bitmap + queue; the sum of their c0
 // is returned in every lane.
 template <bool SM>
-__device__ u64 msps_closure(const Sim<SM> &g, u32 t, u32 wslot, volatile u32 *tail, u64 &bytes) {
+__device__ u64 msps_closure(const Sim<SM> &g, const uint4 &sr, u32 wslot, volatile u32 *tail, u64 &bytes) {
   const u32 lane = threadIdx.x & 31;
   const u32 bm = g.L.msps_bm + wslot * g.L.msps_words;
   const u32 q = g.L.msps_q + wslot * (g.L.n + 1);
@@ -126,8 +84,7 @@ __device__ u64 msps_closure(const Sim<SM> &g, u32 t, u32 wslot, volatile u32 *ta
     u32 pos = atomicAdd((u32 *)tail, 1u);
     g.m.w(q + pos) = p;
   };
-  const uint4 st = g.srec(t);
-  for (u32 j = lane; j < st.w; j += 32) visit(g.par(st.z + j));
+  for (u32 j = lane; j < sr.w; j += 32) visit(g.par(sr.z + j));
   __syncwarp();
   u32 head = 0, tl = *tail;
   __syncwarp();
@@ -220,84 +177,99 @@ __device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t,
     u32 L = g.la(t);
     nbr_components<SM, H == H_DTR_EQ>(g, t, sr, sum, L, bytes);
     stale_score((u64)sr.y + sum, sr.x, L, cmd.clock, c.num, c.den);
-    bytes += 4 + 16 + 4 + 8;
+    bytes += 16 + 4 + 8;          // srec, la, crec
   } else if constexpr (H == H_LRU) {
     stale_score(1, 1, g.la(t), cmd.clock, c.num, c.den);
-    bytes += 8;
+    bytes += 4;
   } else if constexpr (H == H_SIZE) {
     c.num = 1; c.den = g.srec(t).x;
-    bytes += 8;
+    bytes += 4;
   } else if constexpr (H == H_LOCAL) {
     const uint4 sr = g.srec(t);
     stale_score((u64)sr.y, sr.x, g.la(t), cmd.clock, c.num, c.den);
-    bytes += 4 + 16 + 4;
+    bytes += 12;
   } else {
     c.num = splitmix64(cmd.seed ^ (cmd.decisions << 32) ^ (u64)t); c.den = 1;
     bytes += 4;
   }
 }
 
-template <bool SM, int H>
+// Score this thread's share of the pool, K candidates at a time (independent
+// chains in flight), into best.  BM: scan tensor ids rank, rank + size, ... <
+// n_ids and take the pool members (bitmap); else take pool_ids[rank + j*size].
+template <bool SM, bool BM, int H, u32 K>
 __device__ __forceinline__ void score_loop(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, Cand &best,
                                            u32 &bk, u64 &bytes, u64 &evals) {
-  const u32 P = cmd.pool_size;
+  const u32 n = BM ? cmd.n_ids : cmd.pool_size;
   u32 i = rank;
-  for (; i + size < P; i += 2 * size) {            // two independent candidates in flight
-    const u32 t0 = g.pool_ids(i), t1 = g.pool_ids(i + size);
-    Cand c0, c1;
-    score_h<SM, H>(g, cmd, t0, c0, bytes);
-    score_h<SM, H>(g, cmd, t1, c1, bytes);
-    cand_take(best, bk, c0);
-    cand_take(best, bk, c1);
-    evals += 2;
-  }
-  if (i < P) {
-    Cand c0;
-    score_h<SM, H>(g, cmd, g.pool_ids(i), c0, bytes);
-    cand_take(best, bk, c0);
-    evals++;
+  while (i < n) {
+    u32 cand[K];
+    u32 k = 0;
+    while (k < K && i < n) {
+      if constexpr (BM) { if (g.in_pool(i)) cand[k++] = i; }
+      else { cand[k++] = g.pool_ids(i); bytes += 4; }
+      i += size;
+    }
+    Cand c[K];
+#pragma unroll
+    for (u32 r = 0; r < K; r++)
+      if (r < k) score_h<SM, H>(g, cmd, cand[r], c[r], bytes);
+#pragma unroll
+    for (u32 r = 0; r < K; r++)
+      if (r < k) cand_take(best, bk, c[r]);
+    evals += k;
   }
 }
 
 // Score every pool member of this thread's slice; return the slice argmin and
 // its key.  rank/size: thread index in the team; wrank/wsize: warp index (MSPS).
-template <bool SM>
+// WIDE: global-memory team (four candidates in flight per thread, else two).
+template <bool SM, bool BM, bool WIDE = false>
 __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, u32 wrank, u32 wsize,
                            volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk) {
   Cand best = cand_none();
   bk = KEY_NONE;
+  if (BM && rank == 0) bytes += (cmd.n_ids + 7) / 8;     // the pool bitmap
+  constexpr u32 K = WIDE ? 4 : 2;
   switch (cmd.heur) {
-    case H_DTR: score_loop<SM, H_DTR>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_DTR_EQ: score_loop<SM, H_DTR_EQ>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_LRU: score_loop<SM, H_LRU>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_SIZE: score_loop<SM, H_SIZE>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_LOCAL: score_loop<SM, H_LOCAL>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_RANDOM: score_loop<SM, H_RANDOM>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_DTR: score_loop<SM, BM, H_DTR, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_DTR_EQ: score_loop<SM, BM, H_DTR_EQ, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_LRU: score_loop<SM, BM, H_LRU, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_SIZE: score_loop<SM, BM, H_SIZE, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_LOCAL: score_loop<SM, BM, H_LOCAL, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_RANDOM: score_loop<SM, BM, H_RANDOM, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
     default: break;
   }
   // H_MSPS: one warp per candidate
-  const u32 P = cmd.pool_size;
   const u32 nw = wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
   if (wrank >= nw) return best;
   const u32 lane = threadIdx.x & 31;
-  for (u32 i = wrank; i < P; i += nw) {
-    const u32 t = g.pool_ids(i);
-    const u64 sum = msps_closure(g, t, wrank, msps_tail + (threadIdx.x >> 5), bytes);
-    if (lane == 0) {
+  u32 seen = 0;
+  const u32 nscan = BM ? (cmd.n_ids + 31) / 32 : cmd.pool_size;
+  for (u32 w = BM ? 0 : wrank; w < nscan; w += BM ? 1 : nw) {
+    u32 bits = BM ? g.pool_word(w) : 1u;
+    while (bits) {
+      const u32 b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (BM && (seen++ % nw) != wrank) continue;
+      const u32 t = BM ? w * 32 + b : g.pool_ids(w);
       const uint4 sr = g.srec(t);
-      Cand c;
-      c.num = (u64)sr.y + sum;
-      c.den = sr.x;
-      c.id = t;
-      bytes += 4 + 16;
-      evals++;
-      cand_take(best, bk, c);
+      const u64 sum = msps_closure(g, sr, wrank, msps_tail + (threadIdx.x >> 5), bytes);
+      if (lane == 0) {
+        Cand c;
+        c.num = (u64)sr.y + sum;
+        c.den = sr.x;
+        c.id = t;
+        bytes += 16;
+        evals++;
+        cand_take(best, bk, c);
+      }
     }
   }
   return best;
 }
 
-// per-call OP_SCORES: write every pool member's score (MSPS included)
+// per-call OP_SCORES (compact pool): write every pool member's score (MSPS included)
 template <bool SM>
 __device__ void team_scores_out(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, volatile u32 *msps_tail,
                                 u64 *onum, u64 *oden, u32 *oid) {
@@ -309,16 +281,24 @@ __device__ void team_scores_out(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 
     if (wr >= nw) return;
     for (u32 i = wr; i < P; i += nw) {
       const u32 t = g.pool_ids(i);
-      const u64 sum = msps_closure(g, t, wr, msps_tail + (threadIdx.x >> 5), junk);
-      if (lane == 0) { const uint4 sr = g.srec(t); onum[i] = (u64)sr.y + sum; oden[i] = sr.x; oid[i] = t; }
+      const uint4 sr = g.srec(t);
+      const u64 sum = msps_closure(g, sr, wr, msps_tail + (threadIdx.x >> 5), junk);
+      if (lane == 0) { onum[i] = (u64)sr.y + sum; oden[i] = sr.x; oid[i] = t; }
     }
     return;
   }
   for (u32 i = rank; i < P; i += size) {
     const u32 t = g.pool_ids(i);
-    u64 num, den;
-    score_one(g, cmd.heur, cmd.clock, cmd.seed, cmd.decisions, t, num, den, junk);
-    onum[i] = num; oden[i] = den; oid[i] = t;
+    Cand c;
+    switch (cmd.heur) {
+      case H_DTR: score_h<SM, H_DTR>(g, cmd, t, c, junk); break;
+      case H_DTR_EQ: score_h<SM, H_DTR_EQ>(g, cmd, t, c, junk); break;
+      case H_LRU: score_h<SM, H_LRU>(g, cmd, t, c, junk); break;
+      case H_SIZE: score_h<SM, H_SIZE>(g, cmd, t, c, junk); break;
+      case H_LOCAL: score_h<SM, H_LOCAL>(g, cmd, t, c, junk); break;
+      default: score_h<SM, H_RANDOM>(g, cmd, t, c, junk); break;
+    }
+    onum[i] = c.num; oden[i] = c.den; oid[i] = t;
   }
 }
 

@@ -279,3 +279,22 @@ def test_percall_vs_oracle_random(P, oracle_mod):
                 if int(gs["status"]) != 0:
                     break
             assert g.trace().tobytes() == o.trace().tobytes()
+
+
+def test_pool_argmin_standalone(P, oracle_mod):
+    """K3+K4 alone over a stopped grid-engine simulation = the oracle's next decision."""
+    import torch
+    w = models.random_dag(100000, seed=11)
+    v = LogView(w)
+    for h in ("dtr", "dtr_eq", "lru", "size", "msps", "local"):
+        D = 25
+        B = v.peak_total * 97 // 100
+        ref, tr = oracle_mod.replay(w, oracle_mod.HEURISTICS[h], B, max_decisions=D + 1, trace_cap=D + 1)
+        b = P.DeviceBatch([w], [dict(log=0, budget=B, heuristic=P.HEURISTICS[h], max_decisions=D)],
+                          engine=P.ENGINE_GRID)
+        b.run()
+        out = b.pool_argmin().cpu().numpy().astype(np.uint64)
+        torch.cuda.synchronize()
+        nxt = tr[D]
+        assert (int(out[0]), int(out[1]), int(out[2])) == (int(nxt["num"]), int(nxt["den"]), int(nxt["id"])), h
+        assert int(out[4]) > 0
