@@ -1,12 +1,13 @@
 """Build libdtr.so (sm_100a) in-tree with nvcc."""
+import glob
 import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "dtr.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("dtr.cu", "engine.cuh", "leader.cuh")] + \
-       [os.path.join(ROOT, "include", "dtr.h")]
+DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + \
+    [os.path.join(ROOT, "include", "dtr.h")]
 LIB = os.path.join(HERE, "libdtr.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

@@ -450,7 +450,7 @@ struct __align__(16) PaShared {
   u32 msps_tail[PA_THREADS / 32];
 };
 
-__global__ void __launch_bounds__(PA_THREADS, 3) pool_argmin_kernel(const u32 *logw, u32 heur, char *ws,
+__global__ void __launch_bounds__(PA_THREADS, 2) pool_argmin_kernel(const u32 *logw, u32 heur, char *ws,
                                                                     u64 *out /* num, den, id, bytes, evals */) {
   __shared__ PaShared sh;
   __shared__ bool last;

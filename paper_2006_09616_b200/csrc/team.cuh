@@ -194,6 +194,88 @@ __device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t,
   }
 }
 
+// Whole-GPU h_DTR / h_DTR_eq for two candidates at once, in fixed unrolled
+// phases so every load of a phase is independent (in-order issue would
+// otherwise pay one memory latency per neighbour): own records -> all
+// neighbour ids -> all neighbour states (-> UF nodes) -> distinct component
+// records.  Candidates with more than NB neighbours use score_h.
+constexpr u32 NB = 8;
+
+template <bool UF>
+__device__ __forceinline__ void score_pair_dtr(const Sim<false> &g, const Cmd &cmd, const u32 *t, u32 k, Cand *c,
+                                               u64 &bytes) {
+  uint4 sr[2];
+  uint2 cr[2];
+  u32 la[2], deg[2];
+#pragma unroll
+  for (u32 a = 0; a < 2; a++) {
+    if (a < k) { sr[a] = g.srec(t[a]); cr[a] = g.crec(t[a]); la[a] = g.la(t[a]); }
+    else { sr[a] = make_uint4(0, 0, 0, 0); cr[a] = make_uint2(0, 0); la[a] = 0; }
+    deg[a] = sr[a].w + cr[a].y;
+  }
+  u32 q[2][NB];
+#pragma unroll
+  for (u32 a = 0; a < 2; a++)
+#pragma unroll
+    for (u32 j = 0; j < NB; j++)
+      q[a][j] = (a < k && deg[a] <= NB && j < deg[a])
+                    ? (j < sr[a].w ? g.par(sr[a].z + j) : g.m.w(g.L.ch + cr[a].x + (j - sr[a].w))) : NONE;
+  u32 lab[2][NB];
+#pragma unroll
+  for (u32 a = 0; a < 2; a++)
+#pragma unroll
+    for (u32 j = 0; j < NB; j++) lab[a][j] = q[a][j] != NONE ? g.state(q[a][j]) : 0;
+#pragma unroll
+  for (u32 a = 0; a < 2; a++)
+#pragma unroll
+    for (u32 j = 0; j < NB; j++) {
+      const u32 sq = lab[a][j];
+      if constexpr (UF) lab[a][j] = is_evicted(sq) ? g.m.w(g.L.node_of + q[a][j]) : NONE;
+      else lab[a][j] = is_evicted(sq) ? (sq & COMP_MASK) : NONE;
+    }
+  if constexpr (UF) {
+    u32 steps = 0;
+#pragma unroll
+    for (u32 a = 0; a < 2; a++)
+#pragma unroll
+      for (u32 j = 0; j < NB; j++)
+        if (lab[a][j] != NONE) { lab[a][j] = g.uf_root(lab[a][j], steps); bytes += 4; }
+    bytes += 4ull * steps;
+  }
+#pragma unroll
+  for (u32 a = 0; a < 2; a++) {
+    if (a >= k) continue;
+    if (deg[a] > NB) { score_h<false, UF ? H_DTR_EQ : H_DTR>(g, cmd, t[a], c[a], bytes); continue; }
+    u64 sum = 0;
+    u32 L = la[a], nd = 0;
+    u32 cc[NB], cl[NB], ch[NB];
+#pragma unroll
+    for (u32 j = 0; j < NB; j++) {
+      bool first = lab[a][j] != NONE;
+#pragma unroll
+      for (u32 i = 0; i < j; i++) first = first && lab[a][i] != lab[a][j];
+      ch[j] = first ? lab[a][j] : NONE;
+    }
+#pragma unroll
+    for (u32 j = 0; j < NB; j++) {          // distinct component records, all in flight
+      if (ch[j] != NONE) {
+        const uint4 r = UF ? g.uf(ch[j]) : g.comp(ch[j]);
+        cc[j] = r.x; cl[j] = r.z; ch[j] = r.y;   // ch reused: cost high word
+      }
+    }
+#pragma unroll
+    for (u32 j = 0; j < NB; j++) {
+      bool first = lab[a][j] != NONE;
+#pragma unroll
+      for (u32 i = 0; i < j; i++) first = first && lab[a][i] != lab[a][j];
+      if (first) { sum += mk64(cc[j], ch[j]); L = cl[j] > L ? cl[j] : L; nd++; }
+    }
+    c[a].id = t[a];
+    stale_score((u64)sr[a].y + sum, sr[a].x, L, cmd.clock, c[a].num, c[a].den);
+    bytes += 16 + 4 + 8 + 8ull * deg[a] + 12ull * nd;
+  }
+}
+
 // Score this thread's share of the pool, K candidates at a time (independent
 // chains in flight), into best.  BM: scan tensor ids rank, rank + size, ... <
 // n_ids and take the pool members (bitmap); else take pool_ids[rank + j*size].
@@ -211,9 +293,15 @@ __device__ __forceinline__ void score_loop(const Sim<SM> &g, const Cmd &cmd, u32
       i += size;
     }
     Cand c[K];
+    if constexpr (!SM && BM && (H == H_DTR || H == H_DTR_EQ)) {
 #pragma unroll
-    for (u32 r = 0; r < K; r++)
-      if (r < k) score_h<SM, H>(g, cmd, cand[r], c[r], bytes);
+      for (u32 r = 0; r < K; r += 2)
+        if (r < k) score_pair_dtr<H == H_DTR_EQ>(g, cmd, cand + r, k - r < 2 ? k - r : 2, c + r, bytes);
+    } else {
+#pragma unroll
+      for (u32 r = 0; r < K; r++)
+        if (r < k) score_h<SM, H>(g, cmd, cand[r], c[r], bytes);
+    }
 #pragma unroll
     for (u32 r = 0; r < K; r++)
       if (r < k) cand_take(best, bk, c[r]);
@@ -232,8 +320,8 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
   if (BM && rank == 0) bytes += (cmd.n_ids + 7) / 8;     // the pool bitmap
   constexpr u32 K = WIDE ? 4 : 2;
   switch (cmd.heur) {
-    case H_DTR: score_loop<SM, BM, H_DTR, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_DTR_EQ: score_loop<SM, BM, H_DTR_EQ, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_DTR: score_loop<SM, BM, H_DTR, 2>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_DTR_EQ: score_loop<SM, BM, H_DTR_EQ, 2>(g, cmd, rank, size, best, bk, bytes, evals); return best;
     case H_LRU: score_loop<SM, BM, H_LRU, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
     case H_SIZE: score_loop<SM, BM, H_SIZE, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
     case H_LOCAL: score_loop<SM, BM, H_LOCAL, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
