@@ -298,3 +298,23 @@ def test_pool_argmin_standalone(P, oracle_mod):
         nxt = tr[D]
         assert (int(out[0]), int(out[1]), int(out[2])) == (int(nxt["num"]), int(nxt["den"]), int(nxt["id"])), h
         assert int(out[4]) > 0
+
+
+@pytest.mark.parametrize("model", ["transformer", "lstm", "densenet100"])
+def test_grid_engine_all_heuristics(P, oracle_mod, model):
+    """The whole-GPU engine (bitmap pool, paired gathers) on mid-size logs, every heuristic."""
+    w = models.CONFIG_MODELS[model]()
+    v = LogView(w)
+    specs = [dict(log=0, h=h, budget=v.budget(pm), max_decisions=400 if h == "msps" else 1500, seed=3)
+             for h in HS for pm in (250, 900)]
+    assert_parity(P, oracle_mod, [w], specs, 2)
+
+
+def test_config4_lstm_full_size_sample(P, oracle_mod):
+    """Config 4 shape at full size (LSTM T=4096, 2 layers, ~3e5 tensors; budget
+    sized for a ~1e5-tensor pool): the first 300 decisions, whole-GPU engine."""
+    w = models.lstm(T=4096, layers=2)
+    v = LogView(w)
+    B = v.peak_total * 100000 // v.n
+    specs = [dict(log=0, h=h, budget=B, max_decisions=300) for h in ("dtr", "dtr_eq", "lru", "size")]
+    assert_parity(P, oracle_mod, [w], specs, 2)
