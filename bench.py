@@ -201,6 +201,7 @@ def main():
     ap.add_argument("--no-large-pool", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--large-n", type=int, default=1000000)
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-4 / config-5 extra measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -338,6 +339,9 @@ def main():
 
     if rank == 0 and not args.no_large_pool:
         out["roofline_large_pool"] = large_pool(P, torch, dev, args.large_n, hbm_peak, peak_src)
+    if rank == 0 and ws == 1 and not args.no_extra:
+        out["config4_single_run"] = config4(P, torch, dev)
+        out["config5_sweep_sample"] = config5(P, torch, dev)
     if rank == 0 and ws == 1 and not args.no_cpu:
         cores = host_cores()
         dec, ncell, wsec = oracle_sample(logs, specs, budget_s=20.0, cores=cores)
@@ -348,6 +352,60 @@ def main():
         print(json.dumps(out), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def config4(P, torch, dev, cap=100000):
+    """Config 4: one long log, single-run latency on the whole-GPU engine (h_DTR and
+    h_DTR_eq): LSTM T=4096 x 2 layers, budget sized for a ~1e5-tensor pool; the
+    run is bounded at `cap` decisions (a full run makes ~5e5)."""
+    w = models.lstm(T=4096, layers=2)
+    v = LogView(w)
+    B = v.peak_total * 100000 // v.n
+    res = {"workload": f"lstm T=4096 x2 layers, n={v.n} tensors, {v.n_ops} records, B=peak_total*1e5/n, "
+                       f"first {cap} decisions"}
+    for h, name in ((0, "h_DTR"), (1, "h_DTR_eq")):
+        b = P.DeviceBatch([w], [dict(log=0, budget=B, heuristic=h, thrash_kill=16, max_decisions=cap)],
+                          engine=P.ENGINE_GRID)
+        s = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        b.run(s)
+        e1.record(s)
+        torch.cuda.synchronize()
+        r = b.result_rows()[0]
+        ms = e0.elapsed_time(e1)
+        res[name] = {"ms": ms, "status": int(r["status"]), "records_done": int(r["records_done"]),
+                     "decisions": int(r["decisions"]),
+                     "remats": int(r["remats"]), "decisions_per_s": int(r["decisions"]) / ms * 1e3,
+                     "mean_pool": int(r["cand_evals"]) / max(1, int(r["decisions"]))}
+        del b
+    return res
+
+
+def config5(P, torch, dev, cap=2000):
+    """Config 5: the full 900-cell sweep (6 models x 30 budget ratios x {h_DTR,
+    h_DTR_eq, LRU, size, MSPS}) as a bounded sample: every cell stops after `cap`
+    decisions (MSPS on the recurrent logs walks deep evicted closures)."""
+    from paper_2006_09616_b200 import sweep
+    logs = [models.CONFIG_MODELS[m]() for m in ("resnet32", "densenet100", "unet", "lstm", "treelstm", "transformer")]
+    views = [LogView(w) for w in logs]
+    cells = sweep.make_cells(views, models.sweep_permilles(30), ["dtr", "dtr_eq", "lru", "size", "msps"],
+                             max_decisions=cap)
+    rs = sweep.RankSweep(logs, views, sweep.shard(cells, views, 1)[0], device=dev.index)
+    rs.run()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    rs.run(s)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rows = np.concatenate([b.result_rows() for b in rs.batches])
+    dec = int(rows["decisions"].sum())
+    return {"workload": f"900 cells, each capped at {cap} decisions", "ms": ms, "runs_per_s": len(cells) / ms * 1e3,
+            "decisions": dec, "decisions_per_s": dec / ms * 1e3,
+            "cells_at_cap": int((rows["status"] == 8).sum())}
 
 
 def large_pool(P, torch, dev, n, hbm_peak, peak_src, D=1000, reps=20):
@@ -378,8 +436,14 @@ def large_pool(P, torch, dev, n, hbm_peak, peak_src, D=1000, reps=20):
     o = out.cpu().numpy()
     t = sum(ts) / len(ts)
     ach = float(o[3]) / t / 1e9
+    traffic = None
+    try:
+        if n == 1000000:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get("pool_argmin_1e6")
+    except Exception:
+        pass
     return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-            "traffic": None, "peak_source": peak_src, "kernel": "pool_argmin_kernel (K3+K4, h_DTR)",
+            "traffic": traffic, "peak_source": peak_src, "kernel": "pool_argmin_kernel (K3+K4, h_DTR)",
             "workload": f"config5s random locality DAG n={n}, B=0.98*peak_total, pool after {int(row['decisions'])} "
                         f"decisions", "pool": int(o[4]), "bytes_per_launch": int(o[3]),
             "us_per_launch": t * 1e6, "launches": reps, "l2": "flushed before every launch",

@@ -160,7 +160,8 @@ struct Scalars {
   u32 last_rc;        // per-call: result code of the last op
   u32 pending_op;     // per-call: the op word being applied
   u32 n_scores;       // per-call OP_SCORES: pool size scored
-  u32 pad[5];
+  u32 pad[3];
+  u64 kill_limit;     // thrash_kill * base_so_far (recomputed at every MAKE); 0 = off
 };
 
 // ---------------------------------------------------------------------------
@@ -192,6 +193,7 @@ __device__ __forceinline__ bool score_eq(const Cand &a, const Cand &b) {
 
 // lexicographic (score, id): equal scores -> smaller id (reading C-5)
 __device__ __forceinline__ bool cand_less(const Cand &a, const Cand &b) {
+  if (a.num == b.num && a.den == b.den) return a.id < b.id;   // identical rationals (common: size, LRU)
   if (score_less(a, b)) return true;
   if (score_less(b, a)) return false;
   return a.id < b.id;

@@ -329,7 +329,7 @@ struct Leader {
       }
     }
     if (s.clock > CLOCK_LIMIT) { stop(ST_CAPACITY); return false; }
-    if (s.thrash_kill && s.clock > (u64)s.thrash_kill * s.base_so_far) { stop(ST_THRASH); return false; }
+    if (s.kill_limit && s.clock > s.kill_limit) { stop(ST_THRASH); return false; }
     for (u32 j = 0; j < sr.w; j++) release_internal(g.par(sr.z + j));
     s.pb_top = fr.y;
     s.sp--;
@@ -391,6 +391,7 @@ struct Leader {
         for (u32 j = 0; j < sr.w; j++) if (g.rho(g.par(sr.z + j)) == 0) ok = false;   // reading C-12
         if (!ok) { if (!precond()) return CMD_DONE; continue; }
         s.base_so_far += sr.y;
+        s.kill_limit = (u64)s.thrash_kill * s.base_so_far;
         const u32 now = (u32)(s.clock + 1);
         g.state(id) = 0;
         g.la(id) = now;
