@@ -17,9 +17,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "simrd_oracle.c")
 LIB = os.path.join(HERE, "libsimrd_oracle.so")
 
-H_DTR, H_DTR_EQ, H_LRU, H_SIZE, H_MSPS, H_LOCAL, H_RANDOM = range(7)
+H_DTR, H_DTR_EQ, H_LRU, H_SIZE, H_MSPS, H_LOCAL, H_RANDOM, H_DTR_FULL, H_ESTAR = range(9)
 HEURISTICS = {"dtr": H_DTR, "dtr_eq": H_DTR_EQ, "lru": H_LRU, "size": H_SIZE,
-              "msps": H_MSPS, "local": H_LOCAL, "random": H_RANDOM}
+              "msps": H_MSPS, "local": H_LOCAL, "random": H_RANDOM, "dtr_full": H_DTR_FULL, "estar": H_ESTAR}
 OK, PRECOND, OOM, THRASH, CAPACITY, STATE, DECISION_CAP = 0, 2, 3, 4, 5, 6, 8
 
 TRACE_DTYPE = np.dtype([("clock", "<u8"), ("id", "<u4"), ("pad", "<u4"), ("num", "<u8"), ("den", "<u8")])
@@ -63,6 +63,8 @@ def lib():
             L.oracle_scores.argtypes = [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32), u64]
             L.oracle_neighbourhood.restype = u32
             L.oracle_neighbourhood.argtypes = [P, u32, C.POINTER(u32), u32]
+            L.oracle_estar.restype = u32
+            L.oracle_estar.argtypes = [P, u32, C.POINTER(u32), u32]
             L.oracle_state.argtypes = [P, C.POINTER(u64)]
             L.oracle_tensors.argtypes = [P, C.POINTER(C.c_uint8), C.POINTER(u64), C.POINTER(u64),
                                          C.POINTER(C.c_int64)]
@@ -152,6 +154,12 @@ class Runtime:
         cap = 1 << 16
         out = np.zeros(cap, np.uint32)
         k = self.L.oracle_neighbourhood(self.h, int(t), _ptr(out, C.c_uint32), cap)
+        return sorted(int(x) for x in out[:k])
+
+    def estar(self, t):
+        cap = 1 << 16
+        out = np.zeros(cap, np.uint32)
+        k = self.L.oracle_estar(self.h, int(t), _ptr(out, C.c_uint32), cap)
         return sorted(int(x) for x in out[:k])
 
     def state(self):

@@ -23,6 +23,9 @@
  *   h_LRU, h_largest ("size"), h_MSPS
  *   h_DTR_local
  *   h_rand                                                P:1269-1270 (reading C-15)
+ *   h_DTR_full over the DIRECTED e*(t) (ancestors and descendants reached
+ *     through evicted tensors), own staleness
+ *   h_e* "compute-memory" = (c(t) + c0) / m (Theorem 1)
  *
  * Readings of silent / ambiguous points are DESIGN.md's C-1 ... C-19; each is
  * cited where it is applied.  Scores are exact rationals (num, den) of
@@ -41,7 +44,8 @@ enum {
   OR_STATE = 6, OR_DECISION_CAP = 8
 };
 /* ---- heuristic ids (the boundary's values) ---- */
-enum { H_DTR = 0, H_DTR_EQ = 1, H_LRU = 2, H_SIZE = 3, H_MSPS = 4, H_LOCAL = 5, H_RANDOM = 6 };
+enum { H_DTR = 0, H_DTR_EQ = 1, H_LRU = 2, H_SIZE = 3, H_MSPS = 4, H_LOCAL = 5, H_RANDOM = 6,
+       H_DTR_FULL = 7, H_ESTAR = 8 };
 /* ---- log opcodes (dtr_inputs/logfmt.py) ---- */
 enum { OP_MAKE = 1, OP_GET = 2, OP_RELEASE = 3, OP_REMAT = 4, OP_ENSURE = 5, OP_DEBUG_EVICT = 6 };
 
@@ -276,6 +280,28 @@ static uint64_t msps_closure(Sim *s, uint32_t t) {
   return sum;
 }
 
+/* e*(S): the evicted storages that must be resident to compute
+ * S (transitive closure through evicted deps) together with the evicted
+ * storages that need S to be resident (closure through evicted dependents).
+ * Returns the sum of their compute. */
+static uint64_t estar_closure(Sim *s, uint32_t t) {
+  uint64_t sum = msps_closure(s, t);               /* ancestors through evicted parents */
+  s->epoch++;
+  uint32_t qh = 0, qt = 0;
+  s->queue[qt++] = t; s->stamp[t] = s->epoch;
+  while (qh < qt) {                                /* descendants through evicted children */
+    uint32_t x = s->queue[qh++];
+    for (uint32_t j = 0; j < s->C[x].n; j++) {
+      uint32_t c = s->C[x].v[j];
+      if (!evicted(s, c) || s->stamp[c] == s->epoch) continue;
+      s->stamp[c] = s->epoch;
+      s->queue[qt++] = c;
+      sum += s->compute[c];
+    }
+  }
+  return sum;
+}
+
 /* ------------------------------------------------------------------ */
 /* scores: exact rationals (num, den); den = 0 encodes +infinity         */
 /* ------------------------------------------------------------------ */
@@ -341,6 +367,12 @@ static void score(Sim *s, uint32_t t, uint64_t *num, uint64_t *den) {
       return;
     case H_LOCAL:            /* c0 / (m * s) */
       staleness_score(s, s->compute[t], s->mem[t], s->last_access[t], num, den);
+      return;
+    case H_DTR_FULL:         /* (c(S) + sum_{e*(S)} c) / (size(S) * stale(S)) */
+      staleness_score(s, s->compute[t] + estar_closure(s, t), s->mem[t], s->last_access[t], num, den);
+      return;
+    case H_ESTAR:            /* h_e*(t) = (c(t) + c0(f_t)) / m(t) */
+      *num = s->compute[t] + estar_closure(s, t); *den = s->mem[t];
       return;
     case H_RANDOM:           /* X ~ U(0,1) as a counter-based draw (reading C-15) */
       *num = splitmix64(s->seed ^ (s->decisions << 32) ^ (uint64_t)t); *den = 1;
@@ -577,6 +609,29 @@ uint32_t oracle_neighbourhood(Sim *s, uint32_t t, uint32_t *out, uint32_t cap) {
     uint32_t x = s->queue[qh++];
     for (int side = 0; side < 2; side++) {
       vec32 *adj = side ? &s->C[x] : &s->P[x];
+      for (uint32_t j = 0; j < adj->n; j++) {
+        uint32_t y = adj->v[j];
+        if (!evicted(s, y) || s->stamp[y] == s->epoch) continue;
+        s->stamp[y] = s->epoch;
+        s->queue[qt++] = y;
+        if (k < cap) out[k] = y;
+        k++;
+      }
+    }
+  }
+  return k;
+}
+
+/* e*(t) as an explicit set (directed), for the worked-example pins. */
+uint32_t oracle_estar(Sim *s, uint32_t t, uint32_t *out, uint32_t cap) {
+  uint32_t k = 0;
+  for (int dir = 0; dir < 2; dir++) {
+    s->epoch++;
+    uint32_t qh = 0, qt = 0;
+    s->queue[qt++] = t; s->stamp[t] = s->epoch;
+    while (qh < qt) {
+      uint32_t x = s->queue[qh++];
+      vec32 *adj = dir ? &s->C[x] : &s->P[x];
       for (uint32_t j = 0; j < adj->n; j++) {
         uint32_t y = adj->v[j];
         if (!evicted(s, y) || s->stamp[y] == s->epoch) continue;

@@ -66,6 +66,31 @@ def test_worked_example_doc_c_estar(oracle_mod):
     rt = build_fixture(oracle_mod, g)
     for t, exp in g["expect_E"].items():
         assert rt.neighbourhood(int(t)) == exp
+    for t, exp in g["expect_estar"].items():      # the directed e* of the paper's example
+        assert rt.estar(int(t)) == exp
+
+
+def test_estar_directed_differs_from_undirected(oracle_mod):
+    g = gold("simrd_fig_compheur.json")
+    rt = build_fixture(oracle_mod, g)
+    for t, exp in g["expect_directed_estar"].items():
+        assert rt.estar(int(t)) == exp
+
+
+def test_dtr_full_and_estar_scores_hand(oracle_mod):
+    """T_B at clock 7 (la = {t0:3, t2:2, t3:4, t4:4}): directed e*(t0) = {t1, t5, t6}
+    (descendants t1 -> t5 -> t6), e*(t2) = {t1}, e*(t3) = {}, e*(t4) = {t1}.
+    h_DTR_full = (c + sum e*) / (m * (clock - la(t)))  (P:2329-2332);
+    h_e* = (c + sum e*) / m = |e*| + 1 under unit costs."""
+    g = gold("hdtr_T_B_clock7.json")
+    rt = build_fixture(oracle_mod, g, heuristic=oracle_mod.H_DTR_FULL)
+    assert {k: frac(v) for k, v in rt.scores().items()} == {0: Fraction(4, 4), 2: Fraction(2, 5),
+                                                            3: Fraction(1, 3), 4: Fraction(2, 3)}
+    rt = build_fixture(oracle_mod, g, heuristic=oracle_mod.H_ESTAR)
+    sc = rt.scores()
+    assert {k: frac(v) for k, v in sc.items()} == {0: 4, 2: 2, 3: 1, 4: 2}
+    for k in sc:                                    # corollary: |e*| + 1 with unit costs
+        assert frac(sc[k]) == len(rt.estar(k)) + 1
 
 
 def test_hdtr_scores_hand_derived(oracle_mod):
@@ -130,7 +155,7 @@ def test_msps_chain_hand(oracle_mod):
 
 # ---------------------------------------------------------------- closed forms
 
-ALL_H = ["dtr", "dtr_eq", "lru", "size", "msps", "local", "random"]
+ALL_H = ["dtr", "dtr_eq", "lru", "size", "msps", "local", "random", "dtr_full", "estar"]
 
 
 @pytest.mark.parametrize("model", ["resnet32", "unet", "densenet100"])
@@ -226,7 +251,7 @@ def test_bruteforce_random_lower_bound(oracle_mod):
 # ---------------------------------------------------------------- independent twin (ratio staleness)
 
 TWIN_H = {"dtr": TW.H_DTR, "dtr_eq": TW.H_DTR_EQ, "lru": TW.H_LRU, "size": TW.H_SIZE,
-          "msps": TW.H_MSPS, "local": TW.H_LOCAL}
+          "msps": TW.H_MSPS, "local": TW.H_LOCAL, "dtr_full": TW.H_DTR_FULL, "estar": TW.H_ESTAR}
 
 
 @pytest.mark.parametrize("h", list(TWIN_H))

@@ -21,6 +21,7 @@ INF = "inf"
 NEG_INF = None   # last_access := -infinity (banish_V2)
 
 H_DTR, H_DTR_EQ, H_LRU, H_SIZE, H_MSPS, H_LOCAL = range(6)
+H_DTR_FULL, H_ESTAR = 7, 8
 
 
 class OOM(Exception):
@@ -87,6 +88,21 @@ class Twin:
                     stack.append(y)
         return out
 
+    def estar(self, t):
+        """e*(t): evicted ancestors through evicted deps, plus evicted descendants
+        through evicted dependents."""
+        out = set(self.eR(t))
+        seen = {t}
+        stack = [t]
+        while stack:
+            x = stack.pop()
+            for c in self.C[x]:
+                if c not in seen and self.evicted(c):
+                    seen.add(c)
+                    out.add(c)
+                    stack.append(c)
+        return out
+
     def eR(self, t):
         seen = {t}
         stack = [t]
@@ -138,6 +154,11 @@ class Twin:
             return Fraction(self.cost[t] + sum(self.cost[s] for s in self.eR(t)), self.mem[t])
         if self.h == H_LOCAL:
             return self._stale_score(self.cost[t], self.mem[t], self.la[t])
+        if self.h == H_DTR_FULL:
+            num = self.cost[t] + sum(self.cost[s] for s in self.estar(t))
+            return self._stale_score(num, self.mem[t], self.la[t])
+        if self.h == H_ESTAR:
+            return Fraction(self.cost[t] + sum(self.cost[s] for s in self.estar(t)), self.mem[t])
         raise ValueError(self.h)
 
     # -- internal API -------------------------------------------
