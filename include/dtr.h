@@ -51,7 +51,12 @@ typedef enum {
   DTR_H_SIZE = 3,    /* 1 / m(t)              ("GreedyRemat")                            */
   DTR_H_MSPS = 4,    /* (c0(t) + sum_{e_R(t)} c0) / m(t), e_R = evicted ancestors */
   DTR_H_LOCAL = 5,   /* c0(t) / (m(t) s(t))                                      */
-  DTR_H_RANDOM = 6   /* splitmix64(seed ^ decision << 32 ^ id) (reading C-15)      */
+  DTR_H_RANDOM = 6,  /* splitmix64(seed ^ decision << 32 ^ id) (reading C-15)      */
+  DTR_H_DTR_FULL = 7,/* (c0(t) + sum over the DIRECTED e*(t) of c0) / (m(t) s(t)): e* = evicted
+                        ancestors and descendants reached through evicted tensors
+                        (P:934-951); own staleness              */
+  DTR_H_ESTAR = 8    /* h_e* = (c0(t) + sum_{e*(t)} c0) / m(t), Theorem 1's compute-memory
+                        heuristic                                             */
 } dtr_heuristic;
 
 /* ---- log encoding (little-endian uint32 words; see dtr_inputs/logfmt.py) ----

@@ -16,9 +16,9 @@ LIB_PATH = os.environ.get("DTR_LIB") or os.path.join(HERE, "libdtr.so")   # DTR_
 
 DTR_OK, DTR_E_INVAL, DTR_E_PRECOND, DTR_E_OOM, DTR_E_THRASH = 0, 1, 2, 3, 4
 DTR_E_CAPACITY, DTR_E_STATE, DTR_E_CUDA, DTR_E_DECISION_CAP = 5, 6, 7, 8
-H_DTR, H_DTR_EQ, H_LRU, H_SIZE, H_MSPS, H_LOCAL, H_RANDOM = range(7)
+H_DTR, H_DTR_EQ, H_LRU, H_SIZE, H_MSPS, H_LOCAL, H_RANDOM, H_DTR_FULL, H_ESTAR = range(9)
 HEURISTICS = {"dtr": H_DTR, "dtr_eq": H_DTR_EQ, "lru": H_LRU, "size": H_SIZE, "msps": H_MSPS,
-              "local": H_LOCAL, "random": H_RANDOM}
+              "local": H_LOCAL, "random": H_RANDOM, "dtr_full": H_DTR_FULL, "estar": H_ESTAR}
 ENGINE_CTA, ENGINE_GRID = 1, 2
 STATUS_NAMES = {0: "ok", 1: "inval", 2: "precond", 3: "oom", 4: "thrash_killed", 5: "capacity",
                 6: "state", 7: "cuda", 8: "decision_cap"}

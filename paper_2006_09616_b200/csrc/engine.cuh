@@ -43,7 +43,9 @@ constexpr u32 COMP_MASK = (1u << 30) - 1;
 constexpr u32 LIVE_BIT = 1u << 31;           // union-find compaction mark (in uf size)
 constexpr u64 CLOCK_LIMIT = 0xFFFFFFFEull;   // reading C-14: la is stored as clock + 1 in u32
 
-enum { H_DTR = 0, H_DTR_EQ = 1, H_LRU = 2, H_SIZE = 3, H_MSPS = 4, H_LOCAL = 5, H_RANDOM = 6 };
+enum { H_DTR = 0, H_DTR_EQ = 1, H_LRU = 2, H_SIZE = 3, H_MSPS = 4, H_LOCAL = 5, H_RANDOM = 6,
+       H_DTR_FULL = 7, H_ESTAR = 8, H_LAST = 8 };
+__host__ __device__ __forceinline__ bool uses_closure(u32 h) { return h == H_MSPS || h == H_DTR_FULL || h == H_ESTAR; }
 enum { OP_MAKE = 1, OP_GET = 2, OP_RELEASE = 3, OP_REMAT = 4, OP_ENSURE = 5, OP_DEBUG_EVICT = 6,
        OP_SCORES = 7 /* per-call only: score the whole pool */ };
 enum { ST_OK = 0, ST_INVAL = 1, ST_PRECOND = 2, ST_OOM = 3, ST_THRASH = 4, ST_CAPACITY = 5,
@@ -102,7 +104,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
     L.node_of = take(n1);
     L.uf = take(4 * (u64)L.uf_cap);
     L.uf_size = take(L.uf_cap);
-  } else if (heur == H_MSPS) {
+  } else if (uses_closure(heur)) {
     L.msps_warps = msps_warps;
     L.msps_words = (u32)((n1 + 31) / 32);
     L.msps_bm = take((u64)L.msps_words * msps_warps);

@@ -62,11 +62,15 @@ __device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const ui
   bytes += 8ull * nb + 12ull * nd + extra;
 }
 
-// K5: warp-cooperative e_R(t) -- evicted ancestors reached through evicted
-// parents.  Per-warp visited bitmap + queue; the sum of their c0
-// is returned in every lane.
+// K5: warp-cooperative closures.  e_R(t) -- evicted ancestors reached through
+// evicted parents (h_MSPS); with DOWN also the evicted descendants
+// reached through evicted children, i.e. the directed e*(t) of P:2244-2258
+// (h_DTR_full, h_e*).  Ancestors and descendants of t are disjoint in a DAG,
+// so one per-warp visited bitmap + queue serves both passes; the sum of their
+// c0 is returned in every lane.
 template <bool SM>
-__device__ u64 msps_closure(const Sim<SM> &g, const uint4 &sr, u32 wslot, volatile u32 *tail, u64 &bytes) {
+__device__ u64 msps_closure(const Sim<SM> &g, const uint4 &sr, u32 wslot, volatile u32 *tail, u64 &bytes,
+                            u32 t = NONE, bool down = false) {
   const u32 lane = threadIdx.x & 31;
   const u32 bm = g.L.msps_bm + wslot * g.L.msps_words;
   const u32 q = g.L.msps_q + wslot * (g.L.n + 1);
@@ -98,6 +102,25 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &sr, u32 wslot, volati
     head = tl;
     tl = *tail;
     __syncwarp();
+  }
+  if (down) {                                   // evicted descendants through evicted children
+    auto children = [&](u32 x) {
+      const uint2 cr = g.crec(x);
+      bytes += 8;
+      if (!g.L.linked) { for (u32 j = 0; j < cr.y; j++) visit(g.m.w(g.L.ch + cr.x + j)); }
+      else { for (u32 e = cr.x; e != NONE; e = g.m.w(g.L.e_next + e)) visit(g.m.w(g.L.e_child + e)); }
+    };
+    if (lane == 0) children(t);
+    __syncwarp();
+    tl = *tail;
+    __syncwarp();
+    while (head < tl) {
+      for (u32 i = head + lane; i < tl; i += 32) children(g.m.w(q + i));
+      __syncwarp();
+      head = tl;
+      tl = *tail;
+      __syncwarp();
+    }
   }
   for (u32 i = lane; i < tl; i += 32) g.m.w(bm + (g.m.w(q + i) >> 5)) = 0;
   __syncwarp();
@@ -342,12 +365,18 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
       if (BM && (seen++ % nw) != wrank) continue;
       const u32 t = BM ? w * 32 + b : g.pool_ids(w);
       const uint4 sr = g.srec(t);
-      const u64 sum = msps_closure(g, sr, wrank, msps_tail + (threadIdx.x >> 5), bytes);
+      const bool down = cmd.heur != H_MSPS;
+      const u64 sum = msps_closure(g, sr, wrank, msps_tail + (threadIdx.x >> 5), bytes, t, down);
       if (lane == 0) {
         Cand c;
-        c.num = (u64)sr.y + sum;
-        c.den = sr.x;
         c.id = t;
+        if (cmd.heur == H_DTR_FULL) {            // (c(S) + sum_{e*(S)} c) / (size(S) * stale(S))
+          stale_score((u64)sr.y + sum, sr.x, g.la(t), cmd.clock, c.num, c.den);
+          bytes += 4;
+        } else {                                 // MSPS and h_e* (P:1835-1837): (c0 + sum) / m
+          c.num = (u64)sr.y + sum;
+          c.den = sr.x;
+        }
         bytes += 16;
         evals++;
         cand_take(best, bk, c);
@@ -363,15 +392,19 @@ __device__ void team_scores_out(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 
                                 u64 *onum, u64 *oden, u32 *oid) {
   const u32 P = cmd.pool_size;
   u64 junk = 0;
-  if (cmd.heur == H_MSPS) {
+  if (uses_closure(cmd.heur)) {
     const u32 wr = rank >> 5, ws = (size + 31) >> 5, lane = threadIdx.x & 31;
     const u32 nw = ws < g.L.msps_warps ? ws : g.L.msps_warps;
     if (wr >= nw) return;
     for (u32 i = wr; i < P; i += nw) {
       const u32 t = g.pool_ids(i);
       const uint4 sr = g.srec(t);
-      const u64 sum = msps_closure(g, sr, wr, msps_tail + (threadIdx.x >> 5), junk);
-      if (lane == 0) { onum[i] = (u64)sr.y + sum; oden[i] = sr.x; oid[i] = t; }
+      const u64 sum = msps_closure(g, sr, wr, msps_tail + (threadIdx.x >> 5), junk, t, cmd.heur != H_MSPS);
+      if (lane == 0) {
+        u64 num = (u64)sr.y + sum, den = sr.x;
+        if (cmd.heur == H_DTR_FULL) stale_score((u64)sr.y + sum, sr.x, g.la(t), cmd.clock, num, den);
+        onum[i] = num; oden[i] = den; oid[i] = t;
+      }
     }
     return;
   }

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 ROW_FIELDS = ("status", "records_done", "clock", "base", "decisions", "remats", "computations", "peak_M",
               "trace_hash")
-HS = ["dtr", "dtr_eq", "lru", "size", "msps", "local", "random"]
+HS = ["dtr", "dtr_eq", "lru", "size", "msps", "local", "random", "dtr_full", "estar"]
 
 
 @pytest.fixture(scope="module")
@@ -98,7 +98,7 @@ def test_random_programs_wide(P, oracle_mod):
         logs.append(w)
         v = LogView(w)
         for fr in (0.3, 0.6):
-            for h in ("dtr", "dtr_eq", "msps"):
+            for h in ("dtr", "dtr_eq", "msps", "dtr_full", "estar"):
                 specs.append(dict(log=len(logs) - 1, h=h, budget=max(3, int(v.peak_live * fr))))
     assert_parity(P, oracle_mod, logs, specs, 1)
 
@@ -112,7 +112,7 @@ def sweep_specs(v, hs, permilles, log=0, **kw):
 def test_resnet32_sweep(P, oracle_mod):
     w = models.resnet32()
     v = LogView(w)
-    specs = sweep_specs(v, ["dtr", "dtr_eq", "lru", "size", "msps"], models.sweep_permilles(30))
+    specs = sweep_specs(v, ["dtr", "dtr_eq", "lru", "size", "msps", "dtr_full", "estar"], models.sweep_permilles(30))
     assert_parity(P, oracle_mod, [w], specs, 1)
 
 
@@ -238,6 +238,19 @@ def test_percall_hand_fixtures(P):
     assert Fraction(*rt.scores()[2]) == Fraction(6, 4)
 
 
+def test_percall_estar_fixture(P):
+    """Directed e* scores on fixture T_B through the per-call API (hand values, see
+    tests/test_oracle_pins.py::test_dtr_full_and_estar_scores_hand)."""
+    import json, os
+    from fractions import Fraction
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hdtr_T_B_clock7.json")))
+    rt = percall_fixture(P, "dtr_full", g["parents"], g["evict"])
+    assert {k: Fraction(n, d) for k, (n, d) in rt.scores().items()} == {0: 1, 2: Fraction(2, 5), 3: Fraction(1, 3),
+                                                                       4: Fraction(2, 3)}
+    rt = percall_fixture(P, "estar", g["parents"], g["evict"])
+    assert {k: Fraction(n, d) for k, (n, d) in rt.scores().items()} == {0: 4, 2: 2, 3: 1, 4: 2}
+
+
 def test_percall_vs_oracle_random(P, oracle_mod):
     """Random per-call sessions incl. REMAT of evicted tensors and preconditions."""
     rng = np.random.default_rng(7)
@@ -286,7 +299,7 @@ def test_pool_argmin_standalone(P, oracle_mod):
     import torch
     w = models.random_dag(100000, seed=11)
     v = LogView(w)
-    for h in ("dtr", "dtr_eq", "lru", "size", "msps", "local"):
+    for h in ("dtr", "dtr_eq", "lru", "size", "msps", "local", "dtr_full", "estar"):
         D = 25
         B = v.peak_total * 97 // 100
         ref, tr = oracle_mod.replay(w, oracle_mod.HEURISTICS[h], B, max_decisions=D + 1, trace_cap=D + 1)
@@ -305,8 +318,8 @@ def test_grid_engine_all_heuristics(P, oracle_mod, model):
     """The whole-GPU engine (bitmap pool, paired gathers) on mid-size logs, every heuristic."""
     w = models.CONFIG_MODELS[model]()
     v = LogView(w)
-    specs = [dict(log=0, h=h, budget=v.budget(pm), max_decisions=400 if h == "msps" else 1500, seed=3)
-             for h in HS for pm in (250, 900)]
+    specs = [dict(log=0, h=h, budget=v.budget(pm), max_decisions=400 if h in ("msps", "dtr_full", "estar") else 1500,
+                  seed=3) for h in HS for pm in (250, 900)]
     assert_parity(P, oracle_mod, [w], specs, 2)
 
 
