@@ -75,8 +75,9 @@ def lib():
             L.oracle_trace.restype = u64
             L.oracle_trace.argtypes = [P, C.c_void_p, u64]
             L.oracle_replay.restype = i32
-            L.oracle_replay.argtypes = [C.POINTER(u32), u64, i32, u64, u64, u32, u64, i32,
+            L.oracle_replay.argtypes = [C.POINTER(u32), u64, i32, u64, u64, u32, u64, i32, i32,
                                         C.c_void_p, C.c_void_p, u64]
+            L.oracle_set_dealloc.argtypes = [P, i32]
             _lib = L
     return _lib
 
@@ -85,15 +86,18 @@ def _ptr(a, t):
     return a.ctypes.data_as(C.POINTER(t))
 
 
+DEALLOC = {"v2": 0, "v1": 1, "eager": 2, "ignore": 3}
+
+
 def replay(words: np.ndarray, heuristic: int, budget: int, *, seed: int = 0, thrash_kill: int = 16,
-           max_decisions: int = 0, e_mode: int = 0, trace_cap: int = 0):
+           max_decisions: int = 0, e_mode: int = 0, trace_cap: int = 0, dealloc: int = 0):
     """Replay a whole log. Returns (result_row: np.void, trace: np.ndarray)."""
     L = lib()
     w = np.ascontiguousarray(words, dtype=np.uint32)
     res = np.zeros(1, dtype=RESULT_DTYPE)
     tr = np.zeros(max(trace_cap, 1), dtype=TRACE_DTYPE)
     L.oracle_replay(_ptr(w, C.c_uint32), len(w), int(heuristic), int(budget), int(seed),
-                    int(thrash_kill), int(max_decisions), int(e_mode),
+                    int(thrash_kill), int(max_decisions), int(e_mode), int(dealloc),
                     res.ctypes.data_as(C.c_void_p), tr.ctypes.data_as(C.c_void_p), int(trace_cap))
     r = res[0]
     return r, tr[: min(int(r["decisions"]), trace_cap)]
@@ -103,10 +107,11 @@ class Runtime:
     """Per-call oracle runtime mirroring the boundary's dtr_* calls (fixtures, tests)."""
 
     def __init__(self, heuristic=H_DTR, budget=(1 << 62), seed=0, thrash_kill=0, max_decisions=0,
-                 trace_cap=1 << 16, e_mode=0):
+                 trace_cap=1 << 16, e_mode=0, dealloc=0):
         self.L = lib()
         self.h = self.L.oracle_create(int(heuristic), int(budget), int(seed), int(thrash_kill),
                                       int(max_decisions), int(trace_cap), int(e_mode))
+        self.L.oracle_set_dealloc(self.h, int(dealloc))
         self.trace_cap = trace_cap
 
     def __del__(self):

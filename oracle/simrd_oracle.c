@@ -46,6 +46,8 @@ enum {
 /* ---- heuristic ids (the boundary's values) ---- */
 enum { H_DTR = 0, H_DTR_EQ = 1, H_LRU = 2, H_SIZE = 3, H_MSPS = 4, H_LOCAL = 5, H_RANDOM = 6,
        H_DTR_FULL = 7, H_ESTAR = 8 };
+/* ---- deallocation policies ---- */
+enum { DEALLOC_V2 = 0, DEALLOC_V1 = 1, DEALLOC_EAGER = 2, DEALLOC_IGNORE = 3 };
 /* ---- log opcodes (dtr_inputs/logfmt.py) ---- */
 enum { OP_MAKE = 1, OP_GET = 2, OP_RELEASE = 3, OP_REMAT = 4, OP_ENSURE = 5, OP_DEBUG_EVICT = 6 };
 
@@ -66,6 +68,11 @@ static void vpush(vec32 *a, uint32_t x) {
   a->v[a->n++] = x;
 }
 
+static void vremove(vec32 *a, uint32_t x) {
+  for (uint32_t i = 0; i < a->n; i++)
+    if (a->v[i] == x) { memmove(&a->v[i], &a->v[i + 1], (a->n - i - 1) * sizeof(uint32_t)); a->n--; return; }
+}
+
 /* One union-find node: parent pointer, running cost sum, and the
  * max last_access of the set (reading C-9). */
 typedef struct { uint64_t parent; uint64_t cost; int64_t maxla; } uf_node;
@@ -78,6 +85,7 @@ typedef struct {
   uint32_t thrash_kill;       /* reading C-13: abort when clock > kill * base_so_far */
   uint64_t max_decisions;     /* bounded samples: stop after this many decisions */
   int e_mode;                 /* 0: label evicted components once per decision; 1: literal BFS per candidate */
+  int dealloc;                /* DEALLOC_*: what release() does at rho = 0 */
 
   /* tensors t = (P, C, I, m, rho, l) */
   uint32_t n, cap;
@@ -88,6 +96,7 @@ typedef struct {
   uint8_t *computed_once;     /* reading C-19: evicted(x) := !m[x] && computed_once[x] */
   uint64_t *rho, *l;
   uint8_t *in_pool;           /* R.pool as a membership set over tensor ids */
+  uint8_t *banished;          /* V1: permanently evicted and removed from the graph */
 
   /* union-find for h_DTR_eq */
   uint64_t *set_of;           /* T.set: the UF node of each tensor */
@@ -119,6 +128,7 @@ static void grow(Sim *s, uint32_t need) {
 #define RE(f, T) s->f = (T *)realloc(s->f, (size_t)nc * sizeof(T))
   RE(P, vec32); RE(C, vec32); RE(mem, uint64_t); RE(compute, uint64_t); RE(last_access, int64_t);
   RE(m, uint8_t); RE(computed_once, uint8_t); RE(rho, uint64_t); RE(l, uint64_t); RE(in_pool, uint8_t);
+  RE(banished, uint8_t);
   RE(set_of, uint64_t); RE(label, uint32_t); RE(queue, uint32_t); RE(lab_cost, uint64_t);
   RE(lab_maxla, int64_t); RE(stamp, uint32_t);
 #undef RE
@@ -143,7 +153,7 @@ void oracle_destroy(Sim *s) {
   if (!s) return;
   for (uint32_t i = 0; i < s->cap; i++) { free(s->P[i].v); free(s->C[i].v); }
   free(s->P); free(s->C); free(s->mem); free(s->compute); free(s->last_access); free(s->m);
-  free(s->computed_once); free(s->rho); free(s->l); free(s->in_pool); free(s->set_of);
+  free(s->computed_once); free(s->rho); free(s->l); free(s->in_pool); free(s->banished); free(s->set_of);
   free(s->label); free(s->queue); free(s->lab_cost); free(s->lab_maxla); free(s->stamp);
   free(s->uf); free(s->trace); free(s);
 }
@@ -182,7 +192,8 @@ static void uf_union(Sim *s, uint64_t a, uint64_t b) {
 /* pool: t in pool  <=>  t.m = T and t.l = 0                */
 /* ------------------------------------------------------------------ */
 
-static int evicted(const Sim *s, uint32_t x) { return !s->m[x] && s->computed_once[x]; }  /* C-19 */
+/* C-19; a V1-banished tensor is no longer part of the graph */
+static int evicted(const Sim *s, uint32_t x) { return !s->m[x] && s->computed_once[x] && !s->banished[x]; }
 
 /* ------------------------------------------------------------------ */
 /* Evicted neighbourhood E(t): evicted tensors weakly reachable from
@@ -439,10 +450,47 @@ static int free_mem(Sim *s, uint64_t size) {
   return OR_OK;
 }
 
-/* R.release_internal(t), V2 (no banish_V1 branch). */
+/* R.banish_V1(t): evict t if material, pin its children (l + 1,
+ * which takes them out of the pool: pool = {m and l = 0}, reading C-22), and
+ * remove t from the graph; it never re-enters the pool.  A banished evicted
+ * tensor leaves its union-find set like a rematerialized one (its cost is
+ * subtracted, reading C-22). */
+static void banish_v1(Sim *s, uint32_t t) {
+  if (s->m[t]) {
+    s->m[t] = 0;
+    s->M -= s->mem[t];
+    s->in_pool[t] = 0;
+  } else if (s->heuristic == H_DTR_EQ && evicted(s, t)) {
+    uint64_t r = uf_find(s, s->set_of[t]);
+    s->uf[r].cost -= s->compute[t];
+  }
+  s->banished[t] = 1;
+  for (uint32_t j = 0; j < s->C[t].n; j++) {
+    uint32_t c = s->C[t].v[j];
+    s->l[c]++;
+    s->in_pool[c] = 0;
+    vremove(&s->P[c], t);
+  }
+  for (uint32_t j = 0; j < s->P[t].n; j++) vremove(&s->C[s->P[t].v[j]], t);
+  s->C[t].n = 0;
+  s->P[t].n = 0;
+}
+
+/* banish condition: rho = 0 and every child material (the lock
+ * count is not consulted: a lock taken by a pending computation always comes
+ * with a non-material child, and pinned tensors may be banished later,
+ * P:2372-2375). */
+static void maybe_banish_v1(Sim *s, uint32_t t) {
+  if (s->dealloc != DEALLOC_V1 || s->banished[t] || s->rho[t] != 0) return;
+  for (uint32_t j = 0; j < s->C[t].n; j++) if (!s->m[s->C[t].v[j]]) return;
+  banish_v1(s, t);
+}
+
+/* R.release_internal(t). */
 static void release_internal(Sim *s, uint32_t t) {
   s->l[t]--;
-  if (s->l[t] == 0) s->in_pool[t] = 1;
+  if (s->l[t] == 0 && !s->banished[t]) s->in_pool[t] = 1;
+  maybe_banish_v1(s, t);
 }
 
 /* R.get_internal(t). Recursive, depth-first. */
@@ -520,7 +568,7 @@ int oracle_make(Sim *s, uint64_t mem, uint64_t compute, const uint32_t *parents,
   }
   /* Let I := (f.mem, f.compute, R.clock); t := (P, {}, I, bot, 1, 0) */
   s->mem[t] = mem; s->compute[t] = compute; s->last_access[t] = (int64_t)s->clock;
-  s->m[t] = 0; s->computed_once[t] = 0; s->rho[t] = 1; s->l[t] = 0; s->in_pool[t] = 0;
+  s->m[t] = 0; s->computed_once[t] = 0; s->rho[t] = 1; s->l[t] = 0; s->in_pool[t] = 0; s->banished[t] = 0;
   s->set_of[t] = 0;
   s->base_so_far += compute;
   /* foreach p in P: p.C := p.C u {t}; p.I.last_accessed := R.clock */
@@ -549,12 +597,19 @@ int oracle_get(Sim *s, uint32_t t) {
   return OR_OK;
 }
 
-/* R.release(t), V2: rho = 0 -> banish_V2 (last_access := -inf) */
+/* R.release(t).  At rho = 0:
+ *   V2     banish_V2: last_access := -inf
+ *   V1     banish_V1 when every child is material
+ *   eager  evict t normally if it is in the pool
+ *   ignore nothing */
 int oracle_release(Sim *s, uint32_t t) {
   if (sticky(s)) return OR_STATE;
   if (t >= s->n || s->rho[t] == 0) return OR_PRECOND;
   s->rho[t]--;
-  if (s->rho[t] == 0) s->last_access[t] = NEG_INF;
+  if (s->rho[t] != 0) return OR_OK;
+  if (s->dealloc == DEALLOC_V2) s->last_access[t] = NEG_INF;
+  else if (s->dealloc == DEALLOC_V1) maybe_banish_v1(s, t);
+  else if (s->dealloc == DEALLOC_EAGER && s->in_pool[t]) evict(s, t);
   return OR_OK;
 }
 
@@ -586,6 +641,7 @@ int oracle_debug_evict(Sim *s, uint32_t t) {
 }
 
 void oracle_set_budget(Sim *s, uint64_t B) { s->B = B; }
+void oracle_set_dealloc(Sim *s, int policy) { s->dealloc = policy; }
 
 /* Current (num, den) of every pool member, in id order. Returns the count. */
 uint64_t oracle_scores(Sim *s, uint64_t *num, uint64_t *den, uint32_t *ids, uint64_t cap) {
@@ -736,10 +792,11 @@ static void *replay_thread(void *arg) {
  * be as deep as the longest evicted chain, so it runs on a thread with a large
  * stack. */
 int oracle_replay(const uint32_t *words, uint64_t n_words, int heuristic, uint64_t budget,
-                  uint64_t seed, uint32_t thrash_kill, uint64_t max_decisions, int e_mode,
+                  uint64_t seed, uint32_t thrash_kill, uint64_t max_decisions, int e_mode, int dealloc,
                   or_result *res, or_trace_rec *trace, uint64_t trace_cap) {
   if (n_words < 16 || words[0] != 0x4C525444u) return OR_PRECOND;
   Sim *s = oracle_create(heuristic, budget, seed, thrash_kill, max_decisions, trace_cap, e_mode);
+  s->dealloc = dealloc;
   memset(res, 0, sizeof(*res));
   replay_args a = { s, words, n_words, res, 0 };
   pthread_attr_t attr;

@@ -411,3 +411,96 @@ def test_determinism(oracle_mod):
         a, ta = oracle_mod.replay(w, oracle_mod.HEURISTICS[h], v.budget(400), trace_cap=10 ** 6)
         b, tb = oracle_mod.replay(w, oracle_mod.HEURISTICS[h], v.budget(400), trace_cap=10 ** 6)
         assert a.tobytes() == b.tobytes() and ta.tobytes() == tb.tobytes()
+
+
+# ---------------------------------------------------------------- deallocation policies (NEXT #2)
+
+def test_gap_lemma_estar(oracle_mod):
+    """After the forward pass of the linear net with B = 2*ceil(sqrt N), h_e* leaves
+    resident tensors no more than 2(N-2)/(B-1) apart; h_DTR_full / LRU do not."""
+    g = gold("theorem1_estar_v1.json")
+    for N in g["Ns"]:
+        B = 2 * math.ceil(math.sqrt(N))
+        gaps = {}
+        for h in ("estar", "lru"):
+            rt = oracle_mod.Runtime(oracle_mod.HEURISTICS[h], budget=B, dealloc=1)
+            t = rt.compute(1, 1, [])[1]
+            for i in range(2, N + 1):
+                t = rt.compute(1, 1, [t])[1]
+            fl, *_ = rt.tensors()
+            pts = [-1] + [i for i in range(N) if fl[i] & 1]     # the input t0 is always resident
+            gaps[h] = max(b - a for a, b in zip(pts, pts[1:]))
+        assert gaps["estar"] <= 2 * (N - 2) / (B - 1), (N, gaps)
+        if N >= 64:
+            assert gaps["lru"] > 2 * (N - 2) / (B - 1)
+
+
+def test_theorem1_estar_v1(oracle_mod):
+    """Theorem 1 with V1 banishing: h_e* needs O(N) operations at
+    B = 2*ceil(sqrt N) -- C(N)/2N stays below a constant while LRU grows."""
+    g = gold("theorem1_estar_v1.json")
+    for N in g["Ns"]:
+        B = 2 * math.ceil(math.sqrt(N))
+        r, _ = oracle_mod.replay(models.linear(N), oracle_mod.H_ESTAR, B, thrash_kill=0, dealloc=1)
+        assert r["status"] == 0 and int(r["clock"]) / (2 * N) <= g["ratio_bound"], (N, int(r["clock"]))
+        if N >= g["lru_exceeds_from"]:
+            r, _ = oracle_mod.replay(models.linear(N), oracle_mod.H_LRU, B, thrash_kill=0, dealloc=1)
+            assert int(r["clock"]) / (2 * N) > g["ratio_bound"]
+
+
+def test_v1_banish_semantics(oracle_mod):
+    """banish_V1: t0 = f(); t1 = f(t0); release(t0) with its only child
+    material -> t0 evicted (M drops), t1 pinned (out of the pool), t0 gone from the
+    graph; a banished tensor never returns to the pool."""
+    rt = oracle_mod.Runtime(oracle_mod.H_DTR, dealloc=1)
+    rt.compute(1, 1, [])
+    rt.compute(1, 1, [0])
+    assert rt.state()["M"] == 2
+    assert rt.release(0) == 0
+    fl, rho, ell, la = rt.tensors()
+    assert rt.state()["M"] == 1
+    assert (fl[0] & 1) == 0 and (fl[0] & 4) == 0          # not material, not in pool
+    assert (fl[1] & 4) == 0 and ell[1] == 1                # pinned
+    rt.compute(1, 1, [1])                                  # t2 = f(t1): t1 stays pinned
+    fl, rho, ell, la = rt.tensors()
+    assert (fl[1] & 4) == 0 and (fl[2] & 4) == 4
+    # not banished while a child is evicted: t3 = f(t2), t4 = f(t3); evict t3; release t2
+    rt2 = oracle_mod.Runtime(oracle_mod.H_DTR, dealloc=1)
+    for ps in ([], [0], [1]):
+        rt2.compute(1, 1, ps)
+    rt2.debug_evict(1)
+    assert rt2.release(0) == 0
+    fl, *_ = rt2.tensors()
+    assert fl[0] & 1                                      # kept: child t1 is evicted
+
+
+def test_eager_and_ignore_semantics(oracle_mod):
+    """eager eviction: the last release evicts a pool member
+    normally (it stays rematerializable); ignore: release changes nothing."""
+    rt = oracle_mod.Runtime(oracle_mod.H_DTR, dealloc=2)
+    rt.compute(1, 1, [])
+    rt.compute(1, 1, [0])
+    rt.release(0)
+    fl, rho, ell, la = rt.tensors()
+    assert (fl[0] & 3) == 2 and rt.state()["M"] == 1      # evicted, computed once
+    assert rt.rematerialize(0) == 0 and rt.state()["remats"] == 1
+    rt = oracle_mod.Runtime(oracle_mod.H_DTR, dealloc=3)
+    rt.compute(1, 1, [])
+    before = rt.tensors()[3][0]
+    rt.release(0)
+    fl, rho, ell, la = rt.tensors()
+    assert fl[0] & 1 and la[0] == before and rt.state()["M"] == 1
+
+
+@pytest.mark.parametrize("dealloc", ["v1", "eager", "ignore"])
+def test_twin_agrees_dealloc(oracle_mod, dealloc):
+    for h in ("dtr", "dtr_eq", "lru", "dtr_full", "estar"):
+        for s in range(12):
+            w = models.random_program(40, seed=700 + s, p_release=0.35)
+            v = LogView(w)
+            B = max(4, v.peak_live * 6 // 10)
+            tw, status = TW.replay_log(v, TWIN_H[h], B, dealloc=dealloc)
+            r, tr = oracle_mod.replay(w, oracle_mod.HEURISTICS[h], B, thrash_kill=0, trace_cap=10 ** 5,
+                                      dealloc=oracle_mod.DEALLOC[dealloc])
+            assert {0: "ok", oracle_mod.OOM: "oom"}[int(r["status"])] == status
+            assert [(int(x["clock"]), int(x["id"])) for x in tr] == tw.trace, (h, s)

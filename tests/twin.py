@@ -33,8 +33,10 @@ class Thrash(Exception):
 
 
 class Twin:
-    def __init__(self, heuristic=H_DTR, budget=1 << 62, thrash_kill=0):
+    def __init__(self, heuristic=H_DTR, budget=1 << 62, thrash_kill=0, dealloc="v2"):
         self.h = heuristic
+        self.dealloc = dealloc
+        self.banished = []
         self.B = budget
         self.kill = thrash_kill
         self.P, self.C = [], []
@@ -73,7 +75,7 @@ class Twin:
 
     # -- metadata ----------------------------------------------------------
     def evicted(self, x):
-        return (not self.m[x]) and self.once[x]
+        return (not self.m[x]) and self.once[x] and not self.banished[x]
 
     def E(self, t):
         seen = {t}
@@ -189,8 +191,32 @@ class Twin:
 
     def release_internal(self, t):
         self.l[t] -= 1
-        if self.l[t] == 0:
+        if self.l[t] == 0 and not self.banished[t]:
             self.pool.add(t)
+        self.maybe_banish(t)
+
+    def maybe_banish(self, t):
+        """V1: rho = 0 and every child material -> banish."""
+        if self.dealloc != "v1" or self.banished[t] or self.rho[t] != 0:
+            return
+        if not all(self.m[c] for c in self.C[t]):
+            return
+        if self.m[t]:
+            self.m[t] = False
+            self.M -= self.mem[t]
+            self.pool.discard(t)
+        elif self.h == H_DTR_EQ and self.evicted(t):
+            r = self.find(self.set_of[t])
+            self.uf[r][1] -= self.cost[t]
+        self.banished[t] = True
+        for c in self.C[t]:
+            self.l[c] += 1
+            self.pool.discard(c)
+            self.P[c].remove(t)
+        for p in self.P[t]:
+            self.C[p].remove(t)
+        self.C[t] = []
+        self.P[t] = []
 
     def get_internal(self, t):
         if self.m[t]:
@@ -243,6 +269,7 @@ class Twin:
         self.rho.append(1)
         self.l.append(0)
         self.set_of.append(None)
+        self.banished.append(False)
         self.base += cost
         for p in ps:
             self.C[p].append(t)
@@ -261,8 +288,14 @@ class Twin:
     def release(self, t):
         assert self.rho[t] > 0
         self.rho[t] -= 1
-        if self.rho[t] == 0:
+        if self.rho[t] != 0:
+            return
+        if self.dealloc == "v2":
             self.la[t] = NEG_INF
+        elif self.dealloc == "v1":
+            self.maybe_banish(t)
+        elif self.dealloc == "eager" and t in self.pool:
+            self.evict(t)
 
     def rematerialize(self, t):
         assert not self.m[t]
@@ -286,11 +319,11 @@ def _key(s):
     return (1, 0) if s == INF else (0, s)
 
 
-def replay_log(view, heuristic, budget, thrash_kill=0, chooser=None):
+def replay_log(view, heuristic, budget, thrash_kill=0, chooser=None, dealloc="v2"):
     """Replay a decoded log (dtr_inputs.LogView). Returns (twin, status)."""
     from dtr_inputs.logfmt import (OP_MAKE, OP_GET, OP_RELEASE, OP_REMAT, OP_ENSURE, OP_DEBUG_EVICT,
                                    OP_SHIFT, ID_MASK)
-    tw = Twin(heuristic, budget, thrash_kill)
+    tw = Twin(heuristic, budget, thrash_kill, dealloc)
     tw.chooser = chooser
     status = "ok"
     try:
