@@ -512,12 +512,12 @@ static int get_internal(Sim *s, uint32_t t) {
   int rc = OR_OK;
   for (uint32_t j = 0; j < nt && rc == OR_OK; j++) rc = get_internal(s, pt[j]);
   for (uint32_t j = 0; j < nb && rc == OR_OK; j++) rc = get_internal(s, pb[j]);
-  free(pt); free(pb);
-  if (rc != OR_OK) return rc;
-  if (s->M + s->mem[t] > s->B) {
-    rc = free_mem(s, s->mem[t]);
-    if (rc != OR_OK) return rc;
-  }
+  free(pb);
+  if (rc == OR_OK && s->M + s->mem[t] > s->B) rc = free_mem(s, s->mem[t]);
+  if (rc != OR_OK) { free(pt); return rc; }
+  /* the parents locked above, in t.P order: a V1 banish inside the release
+   * loop removes that parent from t.P, so iterate a copy (reading C-22) */
+  for (uint32_t j = 0; j < np; j++) pt[j] = s->P[t].v[j];
   s->m[t] = 1;
   s->l[t] = 1;
   s->M += s->mem[t];
@@ -536,9 +536,10 @@ static int get_internal(Sim *s, uint32_t t) {
     s->computed_once[t] = 1;
     if (s->heuristic == H_DTR_EQ) s->set_of[t] = uf_new_empty(s);   /* P:2312-2313 */
   }
-  if (s->clock > CLOCK_LIMIT) return OR_CAPACITY;
-  if (s->thrash_kill && s->clock > (uint64_t)s->thrash_kill * s->base_so_far) return OR_THRASH;
-  for (uint32_t j = 0; j < np; j++) release_internal(s, s->P[t].v[j]);
+  if (s->clock > CLOCK_LIMIT) { free(pt); return OR_CAPACITY; }
+  if (s->thrash_kill && s->clock > (uint64_t)s->thrash_kill * s->base_so_far) { free(pt); return OR_THRASH; }
+  for (uint32_t j = 0; j < np; j++) release_internal(s, pt[j]);
+  free(pt);
   return OR_OK;
 }
 
@@ -616,7 +617,7 @@ int oracle_release(Sim *s, uint32_t t) {
 /* R.rematerialize(t): precondition t.m = bot */
 int oracle_rematerialize(Sim *s, uint32_t t) {
   if (sticky(s)) return OR_STATE;
-  if (t >= s->n || s->m[t] || !s->computed_once[t]) return OR_PRECOND;
+  if (t >= s->n || s->m[t] || !s->computed_once[t] || s->banished[t]) return OR_PRECOND;  /* C-22 */
   int rc = get_internal(s, t);
   if (rc != OR_OK) return finish(s, rc);
   release_internal(s, t);
@@ -626,7 +627,7 @@ int oracle_rematerialize(Sim *s, uint32_t t) {
 /* Output condition (reading C-11): get_internal(t) with no matching release. */
 int oracle_ensure(Sim *s, uint32_t t) {
   if (sticky(s)) return OR_STATE;
-  if (t >= s->n || !s->computed_once[t]) return OR_PRECOND;
+  if (t >= s->n || !s->computed_once[t] || s->banished[t]) return OR_PRECOND;  /* C-22 */
   int rc = get_internal(s, t);
   if (rc != OR_OK) return finish(s, rc);
   return OR_OK;
@@ -711,7 +712,7 @@ void oracle_state(const Sim *s, uint64_t *scalars /* [8] */) {
 /* per-tensor flags: bit0 m, bit1 computed_once, bit2 in_pool; plus rho, l, last_access */
 void oracle_tensors(const Sim *s, uint8_t *flags, uint64_t *rho, uint64_t *l, int64_t *la) {
   for (uint32_t t = 0; t < s->n; t++) {
-    flags[t] = (uint8_t)(s->m[t] | (s->computed_once[t] << 1) | (s->in_pool[t] << 2));
+    flags[t] = (uint8_t)(s->m[t] | (s->computed_once[t] << 1) | (s->in_pool[t] << 2) | (s->banished[t] << 3));
     rho[t] = s->rho[t]; l[t] = s->l[t]; la[t] = s->last_access[t];
   }
 }

@@ -474,6 +474,71 @@ def test_v1_banish_semantics(oracle_mod):
     assert fl[0] & 1                                      # kept: child t1 is evicted
 
 
+def test_v1_banish_inside_release_loop(oracle_mod):
+    """get_internal releases every parent it locked, even when the
+    first release banishes that parent and removes it from t.P:
+    a = f(), b = f(), t = f(a, b); release a, b (t evicted, so neither is banished);
+    rematerialize t -> release_internal(a) banishes a, release_internal(b) banishes b.
+    Both pin t (l = 2) and only t stays resident (M = 1)."""
+    for h in (oracle_mod.H_DTR, oracle_mod.H_DTR_EQ, oracle_mod.H_LRU):
+        rt = oracle_mod.Runtime(h, dealloc=1)
+        rt.compute(1, 1, [])
+        rt.compute(1, 1, [])
+        rt.compute(1, 1, [0, 1])
+        assert rt.debug_evict(2) == 0
+        assert rt.release(0) == 0 and rt.release(1) == 0
+        fl, rho, ell, la = rt.tensors()
+        assert fl[0] & 1 and fl[1] & 1                     # kept: child t is evicted
+        assert rt.rematerialize(2) == 0
+        fl, rho, ell, la = rt.tensors()
+        assert [int(x) & 1 for x in fl] == [0, 0, 1]
+        assert list(map(int, ell)) == [0, 0, 2]
+        assert rt.state()["M"] == 1
+        assert rt.rematerialize(0) == 2 and rt.ensure(1) == 2  # banished: PRECOND (reading C-22)
+
+
+def test_v1_lock_balance(oracle_mod):
+    """After a V1 replay, every lock is a pin: l(t) = #banished parents of t for every
+    tensor still in the graph, pool = {material, l = 0, not banished}, M = sum of material mem."""
+    from dtr_inputs.logfmt import OP_SHIFT, ID_MASK, OP_ENSURE
+    done = 0
+    for s in range(24):
+        w = models.random_program(60, seed=900 + s, p_release=0.4, max_parents=4, n_ensure=0)
+        v = LogView(w)
+        rt = oracle_mod.Runtime(oracle_mod.H_DTR, budget=max(4, v.peak_live * 6 // 10), dealloc=1)
+        rc = 0
+        for word in v.ops:
+            if rc != 0:
+                break
+            op, i = int(word) >> OP_SHIFT, int(word) & ID_MASK
+            if op == 1:
+                rc, t = rt.compute(int(v.mem[i]), int(v.cost[i]), v.parents(i))
+            elif op == 2:
+                rc = rt.get(i)
+            elif op == 3:
+                rc = rt.release(i)
+        if rc == oracle_mod.OOM:
+            continue
+        assert rc == 0
+        done += 1
+        fl, rho, ell, la = rt.tensors()
+        n = len(fl)
+        banished = [bool(fl[t] & 8) for t in range(n)]
+        for t in range(n):
+            if banished[t]:          # banished => released, not material, computed once
+                assert rho[t] == 0 and (fl[t] & 7) == 2
+                continue
+        for t in range(n):
+            if banished[t]:          # its pins depend on which of t and its parent went first
+                assert not fl[t] & 4
+                continue
+            pins = sum(1 for p in v.parents(t) if banished[p])
+            assert int(ell[t]) == pins, (s, t)
+            assert bool(fl[t] & 4) == (bool(fl[t] & 1) and ell[t] == 0)
+        assert rt.state()["M"] == sum(int(v.mem[t]) for t in range(n) if fl[t] & 1)
+    assert done >= 8
+
+
 def test_eager_and_ignore_semantics(oracle_mod):
     """eager eviction: the last release evicts a pool member
     normally (it stays rematerializable); ignore: release changes nothing."""

@@ -249,7 +249,7 @@ class Twin:
                 self.set_of[t] = self.uf_new()
         if self.kill and self.clock > self.kill * self.base:
             raise Thrash()
-        for p in self.P[t]:
+        for p in list(self.P[t]):      # a V1 banish removes p from t.P mid-loop (reading C-22)
             self.release_internal(p)
 
     # -- external API -------------------------------------------
@@ -298,11 +298,12 @@ class Twin:
             self.evict(t)
 
     def rematerialize(self, t):
-        assert not self.m[t]
+        assert not self.m[t] and not self.banished[t]
         self.get_internal(t)
         self.release_internal(t)
 
     def ensure(self, t):
+        assert not self.banished[t]
         self.get_internal(t)
 
 
