@@ -59,6 +59,16 @@ typedef enum {
                         heuristic                                             */
 } dtr_heuristic;
 
+/* ---- deallocation policies: what release(t) does when t.rho drops to 0 ----
+ * (reading C-22) */
+typedef enum {
+  DTR_DEALLOC_V2 = 0,      /* banish_V2: last_access := -inf -- the default       */
+  DTR_DEALLOC_V1 = 1,      /* banish_V1 once every child is material: evict, pin the children,
+                              remove t from the graph       */
+  DTR_DEALLOC_EAGER = 2,   /* evict t normally if it is in the pool */
+  DTR_DEALLOC_IGNORE = 3   /* nothing                                            */
+} dtr_dealloc;
+
 /* ---- log encoding (little-endian uint32 words; see dtr_inputs/logfmt.py) ----
  * header[16]: magic 'DTRL', version 1, n_tensors, n_edges, n_ops, model_id,
  *             base(u64), peak_live(u64), peak_total(u64), seed(u64), max_parents, 0
@@ -110,7 +120,7 @@ typedef struct {
   uint32_t heuristic;      /* dtr_heuristic */
   uint32_t thrash_kill;    /* 0 = off; else stop with DTR_E_THRASH when clock > kill*base */
   uint32_t cell_id;
-  uint32_t reserved;
+  uint32_t dealloc;        /* dtr_dealloc: what release() does at rho = 0 */
 } dtr_cell;
 
 /* Engines: one CTA per simulation (many small runs, K6) or the whole GPU per
@@ -184,7 +194,7 @@ typedef struct {
   uint32_t cap_tensors;    /* preallocated tensor capacity (> 0) */
   uint32_t cap_edges;      /* preallocated parent-edge capacity */
   int device;              /* CUDA device ordinal */
-  uint32_t reserved;
+  uint32_t dealloc;        /* dtr_dealloc */
   void *stream;            /* cudaStream_t for all work (NULL = legacy default) */
 } dtr_config;
 

@@ -20,6 +20,7 @@ H_DTR, H_DTR_EQ, H_LRU, H_SIZE, H_MSPS, H_LOCAL, H_RANDOM, H_DTR_FULL, H_ESTAR =
 HEURISTICS = {"dtr": H_DTR, "dtr_eq": H_DTR_EQ, "lru": H_LRU, "size": H_SIZE, "msps": H_MSPS,
               "local": H_LOCAL, "random": H_RANDOM, "dtr_full": H_DTR_FULL, "estar": H_ESTAR}
 ENGINE_CTA, ENGINE_GRID = 1, 2
+DEALLOC = {"v2": 0, "v1": 1, "eager": 2, "ignore": 3}
 STATUS_NAMES = {0: "ok", 1: "inval", 2: "precond", 3: "oom", 4: "thrash_killed", 5: "capacity",
                 6: "state", 7: "cuda", 8: "decision_cap"}
 
@@ -30,7 +31,7 @@ RESULT_DTYPE = np.dtype([("cell_id", "<u4"), ("status", "<u4"), ("records_done",
                          ("cand_evals", "<u8"), ("score_bytes", "<u8")])
 CELL_DTYPE = np.dtype([("log_offset", "<u8"), ("budget", "<u8"), ("seed", "<u8"), ("max_decisions", "<u8"),
                        ("trace_offset", "<u8"), ("trace_cap", "<u8"), ("heuristic", "<u4"),
-                       ("thrash_kill", "<u4"), ("cell_id", "<u4"), ("reserved", "<u4")])
+                       ("thrash_kill", "<u4"), ("cell_id", "<u4"), ("dealloc", "<u4")])
 assert TRACE_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 88 and CELL_DTYPE.itemsize == 64
 
 # every symbol include/dtr.h declares
@@ -50,7 +51,7 @@ class _Config(C.Structure):
     _fields_ = [("budget", C.c_uint64), ("seed", C.c_uint64), ("max_decisions", C.c_uint64),
                 ("trace_cap", C.c_uint64), ("heuristic", C.c_uint32), ("thrash_kill", C.c_uint32),
                 ("cap_tensors", C.c_uint32), ("cap_edges", C.c_uint32), ("device", C.c_int),
-                ("reserved", C.c_uint32), ("stream", C.c_void_p)]
+                ("dealloc", C.c_uint32), ("stream", C.c_void_p)]
 
 
 def _load():
@@ -136,6 +137,7 @@ def make_cells(log_offsets, specs, trace_caps=None):
         cells[i]["heuristic"] = int(s["heuristic"])
         cells[i]["thrash_kill"] = int(s.get("thrash_kill", 16))
         cells[i]["cell_id"] = int(s.get("cell_id", i))
+        cells[i]["dealloc"] = int(s.get("dealloc", 0))
     return cells, tcur
 
 
@@ -239,9 +241,9 @@ class DeviceBatch:
 
 class Runtime:
     def __init__(self, heuristic=H_DTR, budget=(1 << 62), seed=0, thrash_kill=0, max_decisions=0,
-                 trace_cap=1 << 16, cap_tensors=1 << 12, cap_edges=1 << 14, device=0, stream=None):
+                 trace_cap=1 << 16, cap_tensors=1 << 12, cap_edges=1 << 14, device=0, stream=None, dealloc=0):
         cfg = _Config(budget, seed, max_decisions, trace_cap, heuristic, thrash_kill, cap_tensors, cap_edges,
-                      device, 0, stream)
+                      device, dealloc, stream)
         h = C.c_void_p()
         _check(lib.dtr_create(C.byref(cfg), C.byref(h)), "dtr_create")
         self.h = h

@@ -141,6 +141,7 @@ __device__ void init_scalars(Scalars &s, const dtr_cell &cell) {
   s.heuristic = cell.heuristic;
   s.thrash_kill = cell.thrash_kill;
   s.cell_id = cell.cell_id;
+  s.dealloc = cell.dealloc;
   s.trace_hash = 14695981039346656037ull;
 }
 
@@ -829,7 +830,8 @@ static int rt_launch(dtr_runtime *rt, u32 init, u32 op_word) {
 }
 
 int dtr_create(const dtr_config *cfg, dtr_runtime **out) {
-  if (!cfg || !out || cfg->cap_tensors == 0 || cfg->heuristic > H_LAST) return DTR_E_INVAL;
+  if (!cfg || !out || cfg->cap_tensors == 0 || cfg->heuristic > H_LAST || cfg->dealloc > DEALLOC_IGNORE)
+    return DTR_E_INVAL;
   if (cfg->cap_tensors >= (1u << 29)) return DTR_E_INVAL;
   dtr_runtime *rt = new dtr_runtime();
   rt->cfg = *cfg;
@@ -851,7 +853,7 @@ int dtr_create(const dtr_config *cfg, dtr_runtime **out) {
   Scalars s;
   memset(&s, 0, sizeof s);
   s.B = cfg->budget; s.seed = cfg->seed; s.max_decisions = cfg->max_decisions; s.trace_cap = cfg->trace_cap;
-  s.heuristic = cfg->heuristic; s.thrash_kill = cfg->thrash_kill;
+  s.heuristic = cfg->heuristic; s.thrash_kill = cfg->thrash_kill; s.dealloc = cfg->dealloc;
   s.trace_hash = 14695981039346656037ull;
   e = cudaMemcpyAsync(rt->d_sc, &s, sizeof s, cudaMemcpyHostToDevice, rt->st);
   if (e != cudaSuccess) { dtr_destroy(rt); return cuda_fail(e); }

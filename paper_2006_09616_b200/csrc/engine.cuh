@@ -23,7 +23,7 @@
 //              order, so a warp's candidates are consecutive ids whose (mostly
 //              nearby) neighbours share sectors and L1 lines
 //   state: bit31 material (t.m = T), bit30 computed once (reading C-19),
-//          bits 0..29 label of t's evicted component (h_DTR)
+//          bit29 V1-banished, bits 0..28 label of t's evicted component (h_DTR)
 //   la:    last_access + 1, 0 = -inf (banish_V2)
 //
 // Independent of oracle/ (shares no code with it).
@@ -39,7 +39,8 @@ typedef unsigned __int128 u128;
 constexpr u32 NONE = 0xFFFFFFFFu;
 constexpr u32 M_BIT = 1u << 31;
 constexpr u32 O_BIT = 1u << 30;
-constexpr u32 COMP_MASK = (1u << 30) - 1;
+constexpr u32 B_BIT = 1u << 29;              // V1-banished: removed from the graph
+constexpr u32 COMP_MASK = (1u << 29) - 1;
 constexpr u32 LIVE_BIT = 1u << 31;           // union-find compaction mark (in uf size)
 constexpr u64 CLOCK_LIMIT = 0xFFFFFFFEull;   // reading C-14: la is stored as clock + 1 in u32
 
@@ -48,10 +49,12 @@ enum { H_DTR = 0, H_DTR_EQ = 1, H_LRU = 2, H_SIZE = 3, H_MSPS = 4, H_LOCAL = 5, 
 __host__ __device__ __forceinline__ bool uses_closure(u32 h) { return h == H_MSPS || h == H_DTR_FULL || h == H_ESTAR; }
 enum { OP_MAKE = 1, OP_GET = 2, OP_RELEASE = 3, OP_REMAT = 4, OP_ENSURE = 5, OP_DEBUG_EVICT = 6,
        OP_SCORES = 7 /* per-call only: score the whole pool */ };
+enum { DEALLOC_V2 = 0, DEALLOC_V1 = 1, DEALLOC_EAGER = 2, DEALLOC_IGNORE = 3 };
 enum { ST_OK = 0, ST_INVAL = 1, ST_PRECOND = 2, ST_OOM = 3, ST_THRASH = 4, ST_CAPACITY = 5,
        ST_STATE = 6, ST_DECISION_CAP = 8 };
 
-__host__ __device__ __forceinline__ bool is_evicted(u32 s) { return (s & (M_BIT | O_BIT)) == O_BIT; }
+__host__ __device__ __forceinline__ bool is_evicted(u32 s) { return (s & (M_BIT | O_BIT | B_BIT)) == O_BIT; }
+__host__ __device__ __forceinline__ bool is_banished(u32 s) { return (s & B_BIT) != 0; }
 __host__ __device__ __forceinline__ bool is_material(u32 s) { return (s & M_BIT) != 0; }
 
 // ---------------------------------------------------------------------------
@@ -162,7 +165,8 @@ struct Scalars {
   u32 last_rc;        // per-call: result code of the last op
   u32 pending_op;     // per-call: the op word being applied
   u32 n_scores;       // per-call OP_SCORES: pool size scored
-  u32 pad[3];
+  u32 dealloc;        // DEALLOC_*: what release does at rho = 0 (reading C-22)
+  u32 pad[2];
   u64 kill_limit;     // thrash_kill * base_so_far (recomputed at every MAKE); 0 = off
 };
 

@@ -78,11 +78,64 @@ struct Leader {
     if (l == 0) pool_remove(t);
     g.ell(t) = l + 1;
   }
-  // release_internal, V2
+  // release_internal; V1 retries banishing here
   __device__ __forceinline__ void release_internal(u32 t) {
     u32 l = g.ell(t) - 1;
     g.ell(t) = l;
-    if (l == 0) pool_add(t);
+    if (l == 0 && !is_banished(g.state(t))) pool_add(t);
+    if (s.dealloc == DEALLOC_V1) maybe_banish(t);
+  }
+
+  // ------------------------------------------------------------- V1 banishing (reading C-22)
+  // children of t that exist (created), are not banished, and are not material?
+  __device__ bool child_not_material(u32 t) {
+    const uint2 cr = g.crec(t);
+    bool bad = false;
+    if (!g.L.linked) {
+      for (u32 j = 0; j < cr.y && !bad; j++) {
+        const u32 c = g.m.w(g.L.ch + cr.x + j);
+        if (c >= s.n_alloc) continue;                 // not created yet: not in t.C
+        const u32 sc = g.state(c);
+        if (!is_banished(sc) && !is_material(sc)) bad = true;
+      }
+    } else {
+      for (u32 e = cr.x; e != NONE && !bad; e = g.m.w(g.L.e_next + e)) {
+        const u32 sc = g.state(g.m.w(g.L.e_child + e));
+        if (!is_banished(sc) && !is_material(sc)) bad = true;
+      }
+      // the tensor under creation is already in t.C but not yet linked
+      if (!bad && s.n_alloc > 0 && !(g.state(s.n_alloc - 1) & O_BIT)) {
+        const uint4 sn = g.srec(s.n_alloc - 1);
+        for (u32 j = 0; j < sn.w; j++) if (g.par(sn.z + j) == t) bad = true;
+      }
+    }
+    return bad;
+  }
+  __device__ void maybe_banish(u32 t) {
+    const u32 st = g.state(t);
+    if (is_banished(st) || g.rho(t) != 0 || child_not_material(t)) return;
+    // banish_V1
+    const uint4 sr = g.srec(t);
+    g.state(t) = (st & O_BIT) | B_BIT;
+    if (is_material(st)) {
+      s.M -= sr.x;
+      pool_remove(t);
+    } else if (is_evicted(st)) {                     // leaves its evicted component
+      if (s.heuristic == H_DTR) remat_exact(t, sr, st & COMP_MASK);
+      else if (s.heuristic == H_DTR_EQ) remat_uf(t, sr.y);
+    }
+    auto pin = [&](u32 c) {                           // c.l := c.l + 1 (pinned: out of the pool)
+      if (is_banished(g.state(c))) return;
+      const u32 l = g.ell(c);
+      if (l == 0) pool_remove(c);
+      g.ell(c) = l + 1;
+    };
+    const uint2 cr = g.crec(t);
+    if (!g.L.linked) {
+      for (u32 j = 0; j < cr.y; j++) { const u32 c = g.m.w(g.L.ch + cr.x + j); if (c < s.n_alloc) pin(c); }
+    } else {
+      for (u32 e = cr.x; e != NONE; e = g.m.w(g.L.e_next + e)) pin(g.m.w(g.L.e_child + e));
+    }
   }
 
   // ------------------------------------------------------------- exact components
@@ -422,17 +475,23 @@ struct Leader {
         if (id >= s.n_alloc || g.rho(id) == 0) { if (!precond()) return CMD_DONE; continue; }
         u32 r = g.rho(id) - 1;
         g.rho(id) = r;
-        if (r == 0) {                               // banish_V2
-          u32 old = g.la(id);
-          g.la(id) = 0;
-          if (s.heuristic == H_DTR && is_evicted(g.state(id))) lower_maxla_exact(id, old);
+        if (r == 0) {
+          if (s.dealloc == DEALLOC_V2) {              // banish_V2
+            u32 old = g.la(id);
+            g.la(id) = 0;
+            if (s.heuristic == H_DTR && is_evicted(g.state(id))) lower_maxla_exact(id, old);
+          } else if (s.dealloc == DEALLOC_V1) {
+            maybe_banish(id);
+          } else if (s.dealloc == DEALLOC_EAGER) {   // evict normally if possible
+            if (pool_has(id)) evict(id);
+          }
         }
         finish_op();
         continue;
       }
       if (op == OP_REMAT || op == OP_ENSURE) {
         u32 st = id < s.n_alloc ? g.state(id) : 0;
-        bool bad = op == OP_REMAT ? !is_evicted(st) : !(st & O_BIT);
+        bool bad = op == OP_REMAT ? !is_evicted(st) : (!(st & O_BIT) || is_banished(st));
         if (id >= s.n_alloc || bad) { if (!precond()) return CMD_DONE; continue; }
         root = id; post = op == OP_REMAT;
         start_gi(id);

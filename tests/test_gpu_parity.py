@@ -32,14 +32,15 @@ def oracle_runs(O, logs, specs, trace=True):
     for s in specs:
         r, tr = O.replay(logs[s["log"]], O.HEURISTICS[s["h"]], s["budget"], seed=s.get("seed", 0),
                          thrash_kill=s.get("thrash_kill", 16), max_decisions=s.get("max_decisions", 0),
-                         trace_cap=(1 << 22) if trace else 0)
+                         trace_cap=(1 << 22) if trace else 0, dealloc=O.DEALLOC[s.get("dealloc", "v2")])
         out.append((r, tr))
     return out
 
 
 def gpu_batch(P, logs, specs, engine, trace_caps):
     spec2 = [dict(log=s["log"], budget=s["budget"], heuristic=P.HEURISTICS[s["h"]], seed=s.get("seed", 0),
-                  thrash_kill=s.get("thrash_kill", 16), max_decisions=s.get("max_decisions", 0)) for s in specs]
+                  thrash_kill=s.get("thrash_kill", 16), max_decisions=s.get("max_decisions", 0),
+                  dealloc=P.DEALLOC[s.get("dealloc", "v2")]) for s in specs]
     b = P.DeviceBatch(logs, spec2, engine=engine, trace_caps=trace_caps)
     b.run()
     import torch
@@ -101,6 +102,92 @@ def test_random_programs_wide(P, oracle_mod):
             for h in ("dtr", "dtr_eq", "msps", "dtr_full", "estar"):
                 specs.append(dict(log=len(logs) - 1, h=h, budget=max(3, int(v.peak_live * fr))))
     assert_parity(P, oracle_mod, logs, specs, 1)
+
+
+# ------------------------------------------------------------------ deallocation policies (reading C-22)
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_dealloc_policies_random(P, oracle_mod, engine):
+    """V1 banishing / eager eviction / ignore on random programs, every heuristic."""
+    logs, specs = [], []
+    for s in range(10 if engine == 1 else 3):
+        w = models.random_program(70, seed=3000 + s, p_release=0.35, max_parents=4)
+        logs.append(w)
+        v = LogView(w)
+        for dealloc in ("v1", "eager", "ignore"):
+            for fr in (0.4, 0.7):
+                for h in HS:
+                    specs.append(dict(log=len(logs) - 1, h=h, budget=max(3, int(v.peak_live * fr)), seed=s,
+                                      dealloc=dealloc))
+    rows = assert_parity(P, oracle_mod, logs, specs, engine)
+    assert sum(int(r["decisions"]) for r in rows) > 0
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_dealloc_v1_linear_theorem1(P, oracle_mod, engine):
+    """linear(N) under V1 (App. A's Theorem 1 setting): h_e* and the baselines."""
+    logs, specs = [], []
+    for N in (64, 200):
+        logs.append(models.linear(N))
+        B = 2 * math.ceil(math.sqrt(N))
+        for h in HS:
+            specs.append(dict(log=len(logs) - 1, h=h, budget=B, thrash_kill=0, dealloc="v1"))
+    rows = assert_parity(P, oracle_mod, logs, specs, engine)
+    # Theorem 1 (P:1839-1852) for h_e*: total cost O(N) -- C/2N <= 2 (pinned on the oracle)
+    for sp, r in zip(specs, rows):
+        if sp["h"] == "estar":
+            N = 64 if sp["log"] == 0 else 200
+            assert int(r["status"]) == 0 and int(r["clock"]) <= 4 * N
+
+
+def test_dealloc_models(P, oracle_mod):
+    """V1 / eager / ignore on the resnet32 log at three budgets."""
+    w = models.resnet32()
+    v = LogView(w)
+    specs = [dict(log=0, h=h, budget=v.budget(pm), dealloc=d)
+             for d in ("v1", "eager", "ignore") for h in ("dtr", "dtr_eq", "lru", "estar") for pm in (300, 600, 900)]
+    assert_parity(P, oracle_mod, [w], specs, 1)
+
+
+def test_percall_dealloc_random(P, oracle_mod):
+    """Per-call sessions under every policy: the linked child lists, the tensor
+    under creation blocking V1, REMAT/ENSURE of banished tensors (PRECOND)."""
+    rng = np.random.default_rng(17)
+    for dealloc in ("v1", "eager", "ignore"):
+        for h in HS:
+            for trial in range(3):
+                B = int(rng.integers(6, 14))
+                g = P.Runtime(P.HEURISTICS[h], budget=B, seed=trial, cap_tensors=256, cap_edges=1024,
+                              dealloc=P.DEALLOC[dealloc])
+                o = oracle_mod.Runtime(oracle_mod.HEURISTICS[h], budget=B, seed=trial,
+                                       dealloc=oracle_mod.DEALLOC[dealloc])
+                live = []
+                for step in range(80):
+                    r = rng.random()
+                    if r < 0.55 or not live:
+                        k = int(rng.integers(0, min(3, len(live)) + 1))
+                        ps = [int(x) for x in rng.choice(live, size=k, replace=False)] if k else []
+                        m, c = int(rng.integers(1, 4)), int(rng.integers(1, 5))
+                        a, b = g.compute(m, c, ps), o.compute(m, c, ps)
+                        assert a == b, (dealloc, h, trial, step)
+                        if a[0] == 0:
+                            live.append(a[1])
+                    elif r < 0.8:
+                        t = int(rng.choice(live))
+                        assert g.release(t) == o.release(t)
+                        live.remove(t)
+                    elif r < 0.9:
+                        t = int(rng.integers(0, o.state()["n"] + 2))
+                        assert g.rematerialize(t) == o.rematerialize(t)
+                    else:
+                        t = int(rng.integers(0, o.state()["n"] + 1))
+                        assert g.ensure(t) == o.ensure(t)
+                    gs, os_ = g.stats(), o.result()
+                    for f in ("status", "clock", "decisions", "remats", "computations", "peak_M", "trace_hash"):
+                        assert int(gs[f]) == int(os_[f]), (dealloc, h, trial, step, f)
+                    if int(gs["status"]) != 0:
+                        break
+                assert g.trace().tobytes() == o.trace().tobytes()
 
 
 # ------------------------------------------------------------------ config 2 / 3
