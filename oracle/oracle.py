@@ -20,6 +20,18 @@ LIB = os.path.join(HERE, "libsimrd_oracle.so")
 H_DTR, H_DTR_EQ, H_LRU, H_SIZE, H_MSPS, H_LOCAL, H_RANDOM, H_DTR_FULL, H_ESTAR = range(9)
 HEURISTICS = {"dtr": H_DTR, "dtr_eq": H_DTR_EQ, "lru": H_LRU, "size": H_SIZE,
               "msps": H_MSPS, "local": H_LOCAL, "random": H_RANDOM, "dtr_full": H_DTR_FULL, "estar": H_ESTAR}
+# the D.1 ablation h'(s, m, c) (reading C-23): id = 16 + 4*c + 2*m + s
+ABL_C = ("estar", "eqclass", "local", "no")
+
+
+def abl_id(c: str, m: bool, s: bool) -> int:
+    return 16 + 4 * ABL_C.index(c) + 2 * int(bool(m)) + int(bool(s))
+
+
+for _c in ABL_C:
+    for _m in (0, 1):
+        for _s in (0, 1):
+            HEURISTICS[f"abl_{_c}_{'m' if _m else 'x'}{'s' if _s else 'x'}"] = abl_id(_c, _m, _s)
 OK, PRECOND, OOM, THRASH, CAPACITY, STATE, DECISION_CAP = 0, 2, 3, 4, 5, 6, 8
 
 TRACE_DTYPE = np.dtype([("clock", "<u8"), ("id", "<u4"), ("pad", "<u4"), ("num", "<u8"), ("den", "<u8")])

@@ -26,6 +26,7 @@
  *   h_DTR_full over the DIRECTED e*(t) (ancestors and descendants reached
  *     through evicted tensors), own staleness
  *   h_e* "compute-memory" = (c(t) + c0) / m (Theorem 1)
+ *   the ablation h'(s, m, c)(t) = c(t) / [m(t) s(t)]      P:2527-2536 (reading C-23)
  *
  * Readings of silent / ambiguous points are DESIGN.md's C-1 ... C-19; each is
  * cited where it is applied.  Scores are exact rationals (num, den) of
@@ -46,6 +47,13 @@ enum {
 /* ---- heuristic ids (the boundary's values) ---- */
 enum { H_DTR = 0, H_DTR_EQ = 1, H_LRU = 2, H_SIZE = 3, H_MSPS = 4, H_LOCAL = 5, H_RANDOM = 6,
        H_DTR_FULL = 7, H_ESTAR = 8 };
+/* the D.1 ablation h'(s, m, c): id = H_ABL + 4*c + 2*m + s with
+ * c in {0: e*, 1: EqClass (e~*), 2: local, 3: no}, m, s in {0: no, 1: yes} (reading C-23) */
+enum { H_ABL = 16, H_ABL_END = 32 };
+enum { ABL_C_ESTAR = 0, ABL_C_EQCLASS = 1, ABL_C_LOCAL = 2, ABL_C_NO = 3 };
+static int is_abl(int h) { return h >= H_ABL && h < H_ABL_END; }
+/* heuristics that keep the union-find evicted components */
+static int uses_uf(int h) { return h == H_DTR_EQ || (is_abl(h) && ((h - H_ABL) >> 2) == ABL_C_EQCLASS); }
 /* ---- deallocation policies ---- */
 enum { DEALLOC_V2 = 0, DEALLOC_V1 = 1, DEALLOC_EAGER = 2, DEALLOC_IGNORE = 3 };
 /* ---- log opcodes (dtr_inputs/logfmt.py) ---- */
@@ -334,6 +342,32 @@ static void staleness_score(const Sim *s, uint64_t num, uint64_t mem, int64_t L,
   *on = num; *od = mem * st;
 }
 
+/* e~*(t): the distinct union-find sets of t's evicted deps and
+ * dependents; *sum = their total cost, *L = max(*L, their max last_access). */
+static void eqclass_sum(Sim *s, uint32_t t, uint64_t *sum_out, int64_t *L_out) {
+  uint64_t sum = 0; int64_t L = *L_out;
+  uint64_t roots[2048]; uint32_t nr = 0;          /* distinct adjacent roots */
+  uint64_t *rs = roots; uint64_t *heap = NULL;
+  uint32_t deg = s->P[t].n + s->C[t].n;
+  if (deg > 2048) { heap = (uint64_t *)malloc(deg * sizeof(uint64_t)); rs = heap; }
+  for (int side = 0; side < 2; side++) {
+    vec32 *adj = side ? &s->C[t] : &s->P[t];
+    for (uint32_t j = 0; j < adj->n; j++) {
+      uint32_t y = adj->v[j];
+      if (!evicted(s, y)) continue;
+      uint64_t r = uf_find(s, s->set_of[y]);     /* no unions when querying */
+      int dup = 0;
+      for (uint32_t k = 0; k < nr; k++) if (rs[k] == r) { dup = 1; break; }
+      if (dup) continue;
+      rs[nr++] = r;
+      sum += s->uf[r].cost;
+      if (s->uf[r].maxla > L) L = s->uf[r].maxla;
+    }
+  }
+  free(heap);
+  *sum_out = sum; *L_out = L;
+}
+
 static void score(Sim *s, uint32_t t, uint64_t *num, uint64_t *den) {
   switch (s->heuristic) {
     case H_DTR: {            /* P:100-108 */
@@ -344,26 +378,8 @@ static void score(Sim *s, uint32_t t, uint64_t *num, uint64_t *den) {
       return;
     }
     case H_DTR_EQ: {         /* P:2286-2293; staleness per reading C-9 */
-      uint64_t sum = 0; int64_t L = s->last_access[t];
-      uint64_t roots[2048]; uint32_t nr = 0;          /* distinct adjacent roots */
-      uint64_t *rs = roots; uint64_t *heap = NULL;
-      uint32_t deg = s->P[t].n + s->C[t].n;
-      if (deg > 2048) { heap = (uint64_t *)malloc(deg * sizeof(uint64_t)); rs = heap; }
-      for (int side = 0; side < 2; side++) {
-        vec32 *adj = side ? &s->C[t] : &s->P[t];
-        for (uint32_t j = 0; j < adj->n; j++) {
-          uint32_t y = adj->v[j];
-          if (!evicted(s, y)) continue;
-          uint64_t r = uf_find(s, s->set_of[y]);     /* no unions when querying */
-          int dup = 0;
-          for (uint32_t k = 0; k < nr; k++) if (rs[k] == r) { dup = 1; break; }
-          if (dup) continue;
-          rs[nr++] = r;
-          sum += s->uf[r].cost;
-          if (s->uf[r].maxla > L) L = s->uf[r].maxla;
-        }
-      }
-      free(heap);
+      uint64_t sum; int64_t L = s->last_access[t];
+      eqclass_sum(s, t, &sum, &L);
       staleness_score(s, s->compute[t] + sum, s->mem[t], L, num, den);
       return;
     }
@@ -389,6 +405,20 @@ static void score(Sim *s, uint32_t t, uint64_t *num, uint64_t *den) {
       *num = splitmix64(s->seed ^ (s->decisions << 32) ^ (uint64_t)t); *den = 1;
       return;
   }
+  if (is_abl(s->heuristic)) {  /* h'(s, m, c)(t) = c(t) / [m(t) s(t)]  (reading C-23) */
+    const int code = s->heuristic - H_ABL, cc = code >> 2, use_m = (code >> 1) & 1, use_s = code & 1;
+    uint64_t c = 1;                                            /* c = no: c(t) = 1 */
+    if (cc == ABL_C_ESTAR) c = s->compute[t] + estar_closure(s, t);
+    else if (cc == ABL_C_EQCLASS) {
+      uint64_t sum; int64_t L = s->last_access[t];
+      eqclass_sum(s, t, &sum, &L);                             /* the sets' costs; own staleness */
+      c = s->compute[t] + sum;
+    } else if (cc == ABL_C_LOCAL) c = s->compute[t];
+    const uint64_t m = use_m ? s->mem[t] : 1;                  /* m = no: m(t) = 1 */
+    if (use_s) staleness_score(s, c, m, s->last_access[t], num, den);   /* stale_T(t) */
+    else { *num = c; *den = m; }                               /* s = no: s(t) = 1 */
+    return;
+  }
   *num = 0; *den = 1;
 }
 
@@ -410,7 +440,7 @@ static void evict(Sim *s, uint32_t t) {
   s->m[t] = 0;
   s->M -= s->mem[t];
   s->in_pool[t] = 0;
-  if (s->heuristic == H_DTR_EQ) {
+  if (uses_uf(s->heuristic)) {
     uint64_t r = uf_find(s, s->set_of[t]);
     s->uf[r].cost += s->compute[t];                               /* "+c0(t)" */
     if (s->last_access[t] > s->uf[r].maxla) s->uf[r].maxla = s->last_access[t];
@@ -460,7 +490,7 @@ static void banish_v1(Sim *s, uint32_t t) {
     s->m[t] = 0;
     s->M -= s->mem[t];
     s->in_pool[t] = 0;
-  } else if (s->heuristic == H_DTR_EQ && evicted(s, t)) {
+  } else if (uses_uf(s->heuristic) && evicted(s, t)) {
     uint64_t r = uf_find(s, s->set_of[t]);
     s->uf[r].cost -= s->compute[t];
   }
@@ -526,7 +556,7 @@ static int get_internal(Sim *s, uint32_t t) {
   s->computations++;
   if (s->computed_once[t]) {
     s->remats++;
-    if (s->heuristic == H_DTR_EQ) {
+    if (uses_uf(s->heuristic)) {
       /* "S.set.cost := S.set.cost - cost(S); S.set := empty" */
       uint64_t r = uf_find(s, s->set_of[t]);
       s->uf[r].cost -= s->compute[t];
@@ -534,7 +564,7 @@ static int get_internal(Sim *s, uint32_t t) {
     }
   } else {
     s->computed_once[t] = 1;
-    if (s->heuristic == H_DTR_EQ) s->set_of[t] = uf_new_empty(s);   /* P:2312-2313 */
+    if (uses_uf(s->heuristic)) s->set_of[t] = uf_new_empty(s);   /* P:2312-2313 */
   }
   if (s->clock > CLOCK_LIMIT) { free(pt); return OR_CAPACITY; }
   if (s->thrash_kill && s->clock > (uint64_t)s->thrash_kill * s->base_so_far) { free(pt); return OR_THRASH; }
@@ -577,7 +607,7 @@ int oracle_make(Sim *s, uint64_t mem, uint64_t compute, const uint32_t *parents,
     uint32_t p = s->P[t].v[j];
     vpush(&s->C[p], t);
     s->last_access[p] = (int64_t)s->clock;
-    if (s->heuristic == H_DTR_EQ && evicted(s, p)) {              /* reading C-9 */
+    if (uses_uf(s->heuristic) && evicted(s, p)) {              /* reading C-9 */
       uint64_t r = uf_find(s, s->set_of[p]);
       if ((int64_t)s->clock > s->uf[r].maxla) s->uf[r].maxla = (int64_t)s->clock;
     }

@@ -569,3 +569,79 @@ def test_twin_agrees_dealloc(oracle_mod, dealloc):
                                       dealloc=oracle_mod.DEALLOC[dealloc])
             assert {0: "ok", oracle_mod.OOM: "oom"}[int(r["status"])] == status
             assert [(int(x["clock"]), int(x["id"])) for x in tr] == tw.trace, (h, s)
+
+
+# ---------------------------------------------------------------- D.1 ablation h'(s, m, c) (reading C-23)
+
+def test_ablation_scores_hand(oracle_mod):
+    """Hand scores of h'(s,m,c) = c/(m s) on fixture T_B (tests/golden/ablation_T_B_clock7.json).
+    EqClass and e* differ on t2 and t4: the union-find set of t1 also holds t5 and t6
+    (a phantom connection), the directed e* does not."""
+    g = gold("hdtr_T_B_clock7.json")
+    a = gold("ablation_T_B_clock7.json")
+    for name, exp in a["expect"].items():
+        rt = build_fixture(oracle_mod, g, heuristic=oracle_mod.HEURISTICS["abl_" + name])
+        got = {str(k): frac(v) for k, v in rt.scores().items()}
+        assert got == {k: frac(v) for k, v in exp.items()}, name
+
+
+def _same_trace(O, w, h1, h2, B):
+    r1, t1 = O.replay(w, O.HEURISTICS[h1], B, thrash_kill=0, trace_cap=1 << 20)
+    r2, t2 = O.replay(w, O.HEURISTICS[h2], B, thrash_kill=0, trace_cap=1 << 20)
+    assert int(r1["status"]) == int(r2["status"])
+    assert [(int(x["clock"]), int(x["id"])) for x in t1] == [(int(x["clock"]), int(x["id"])) for x in t2], (h1, h2)
+    return int(r1["decisions"])
+
+
+def test_ablation_reduces_to_named_heuristics(oracle_mod):
+    """P:2527-2536 with measures ablated reduces to heuristics pinned elsewhere:
+    h'(s,m,e*) = h_DTR_full, h'(no s, m, e*) = h_e* (P:1835-1837),
+    h'(s,m,local) = h_DTR_local, h'(s, no m, no c) = LRU,
+    h'(no s, m, no c) = largest-first. The eviction sequences match
+    (the scores themselves may differ by a constant factor)."""
+    pairs = [("abl_estar_ms", "dtr_full"), ("abl_estar_mx", "estar"), ("abl_local_ms", "local"),
+             ("abl_no_xs", "lru"), ("abl_no_mx", "size")]
+    dec = 0
+    for s in range(6):
+        w = models.random_program(80, seed=1300 + s, p_release=0.3, max_parents=4)
+        v = LogView(w)
+        for fr in (0.35, 0.6):
+            for h1, h2 in pairs:
+                dec += _same_trace(oracle_mod, w, h1, h2, max(3, int(v.peak_live * fr)))
+    w = models.resnet32()
+    v = LogView(w)
+    for h1, h2 in pairs:
+        dec += _same_trace(oracle_mod, w, h1, h2, v.budget(400))
+    assert dec > 1000
+
+
+def test_ablation_constant_score_evicts_smallest_id(oracle_mod):
+    """h'(no s, no m, no c) = 1 for every candidate: by the id tie-break (C-5) each
+    decision takes the smallest id in the pool -- the twin with a min-id chooser."""
+    for s in range(8):
+        w = models.random_program(60, seed=1400 + s, p_release=0.3)
+        v = LogView(w)
+        B = max(3, v.peak_live // 2)
+        tw, status = TW.replay_log(v, TW.H_SIZE, B, chooser=lambda tw, c: min(c))
+        r, tr = oracle_mod.replay(w, oracle_mod.HEURISTICS["abl_no_xx"], B, thrash_kill=0, trace_cap=10 ** 5)
+        assert {0: "ok", oracle_mod.OOM: "oom"}[int(r["status"])] == status
+        assert [(int(x["clock"]), int(x["id"])) for x in tr] == tw.trace
+
+
+@pytest.mark.parametrize("c", ["estar", "eqclass", "local", "no"])
+def test_ablation_twin_agrees(oracle_mod, c):
+    """All 16 variants: the C oracle and the Fraction twin (ratio staleness) agree."""
+    for m in "xm":
+        for st in "xs":
+            name = f"abl_{c}_{m}{st}"
+            hid = oracle_mod.HEURISTICS[name]
+            for s in range(8):
+                w = models.random_program(50, seed=1500 + s, p_release=0.3, max_parents=3)
+                v = LogView(w)
+                B = max(4, v.peak_live * 5 // 10)
+                for dealloc in ("v2", "v1"):
+                    tw, status = TW.replay_log(v, hid, B, dealloc=dealloc)
+                    r, tr = oracle_mod.replay(w, hid, B, thrash_kill=0, trace_cap=10 ** 5,
+                                              dealloc=oracle_mod.DEALLOC[dealloc])
+                    assert {0: "ok", oracle_mod.OOM: "oom"}[int(r["status"])] == status
+                    assert [(int(x["clock"]), int(x["id"])) for x in tr] == tw.trace, (name, s, dealloc)

@@ -161,14 +161,31 @@ class Twin:
             return self._stale_score(num, self.mem[t], self.la[t])
         if self.h == H_ESTAR:
             return Fraction(self.cost[t] + sum(self.cost[s] for s in self.estar(t)), self.mem[t])
+        if 16 <= self.h < 32:       # h'(s, m, c) = c / (m * s), ablated measures = 1
+            code = self.h - 16
+            kind, use_m, use_s = code >> 2, (code >> 1) & 1, code & 1
+            if kind == 0:
+                c = self.cost[t] + sum(self.cost[s] for s in self.estar(t))
+            elif kind == 1:
+                roots = {self.find(self.set_of[q]) for q in self.P[t] + self.C[t] if self.evicted(q)}
+                c = self.cost[t] + sum(self.uf[r][1] for r in roots)
+            elif kind == 2:
+                c = self.cost[t]
+            else:
+                c = 1
+            m = self.mem[t] if use_m else 1
+            return self._stale_score(c, m, self.la[t]) if use_s else Fraction(c, m)
         raise ValueError(self.h)
+
+    def uses_uf(self):
+        return self.h == H_DTR_EQ or (16 <= self.h < 32 and (self.h - 16) >> 2 == 1)
 
     # -- internal API -------------------------------------------
     def evict(self, t):
         self.m[t] = False
         self.M -= self.mem[t]
         self.pool.discard(t)
-        if self.h == H_DTR_EQ:
+        if self.uses_uf():
             r = self.find(self.set_of[t])
             self.uf[r][1] += self.cost[t]
             self.uf[r][2] = _max_la(self.uf[r][2], self.la[t])
@@ -205,7 +222,7 @@ class Twin:
             self.m[t] = False
             self.M -= self.mem[t]
             self.pool.discard(t)
-        elif self.h == H_DTR_EQ and self.evicted(t):
+        elif self.uses_uf() and self.evicted(t):
             r = self.find(self.set_of[t])
             self.uf[r][1] -= self.cost[t]
         self.banished[t] = True
@@ -239,13 +256,13 @@ class Twin:
         self.computations += 1
         if self.once[t]:
             self.remats += 1
-            if self.h == H_DTR_EQ:
+            if self.uses_uf():
                 r = self.find(self.set_of[t])
                 self.uf[r][1] -= self.cost[t]
                 self.set_of[t] = self.uf_new()
         else:
             self.once[t] = True
-            if self.h == H_DTR_EQ:
+            if self.uses_uf():
                 self.set_of[t] = self.uf_new()
         if self.kill and self.clock > self.kill * self.base:
             raise Thrash()
@@ -274,7 +291,7 @@ class Twin:
         for p in ps:
             self.C[p].append(t)
             self.la[p] = self.clock
-            if self.h == H_DTR_EQ and self.evicted(p):
+            if self.uses_uf() and self.evicted(p):
                 r = self.find(self.set_of[p])
                 self.uf[r][2] = _max_la(self.uf[r][2], self.clock)
         self.get_internal(t)
