@@ -55,9 +55,17 @@ typedef enum {
   DTR_H_DTR_FULL = 7,/* (c0(t) + sum over the DIRECTED e*(t) of c0) / (m(t) s(t)): e* = evicted
                         ancestors and descendants reached through evicted tensors
                         (P:934-951); own staleness              */
-  DTR_H_ESTAR = 8    /* h_e* = (c0(t) + sum_{e*(t)} c0) / m(t), Theorem 1's compute-memory
+  DTR_H_ESTAR = 8,   /* h_e* = (c0(t) + sum_{e*(t)} c0) / m(t), Theorem 1's compute-memory
                         heuristic                                             */
+  DTR_H_ABL = 16     /* first of the 16 D.1 ablation variants, see DTR_H_ABLATION            */
 } dtr_heuristic;
+
+/* The D.1 ablation h'(s, m, c)(t) = c(t) / [m(t) * s(t)] (DESIGN.md
+ * reading C-23).  c: 0 = e* (c0(t) + sum_{e*(t)} c0), 1 = EqClass (c0(t) + the costs
+ * of the distinct union-find sets of t's evicted deps and dependents),
+ * 2 = local (c0(t)), 3 = no (1); m, s: 1 = size / own staleness, 0 = the constant 1.
+ * The heuristic id is DTR_H_ABLATION(c, m, s), i.e. 16 ... 31. */
+#define DTR_H_ABLATION(c, m, s) (DTR_H_ABL + 4u * (uint32_t)(c) + 2u * (uint32_t)(m) + (uint32_t)(s))
 
 /* ---- deallocation policies: what release(t) does when t.rho drops to 0 ----
  * (reading C-22) */

@@ -19,6 +19,18 @@ DTR_E_CAPACITY, DTR_E_STATE, DTR_E_CUDA, DTR_E_DECISION_CAP = 5, 6, 7, 8
 H_DTR, H_DTR_EQ, H_LRU, H_SIZE, H_MSPS, H_LOCAL, H_RANDOM, H_DTR_FULL, H_ESTAR = range(9)
 HEURISTICS = {"dtr": H_DTR, "dtr_eq": H_DTR_EQ, "lru": H_LRU, "size": H_SIZE, "msps": H_MSPS,
               "local": H_LOCAL, "random": H_RANDOM, "dtr_full": H_DTR_FULL, "estar": H_ESTAR}
+# the D.1 ablation h'(s, m, c) (include/dtr.h DTR_H_ABLATION): id = 16 + 4*c + 2*m + s
+ABL_C = ("estar", "eqclass", "local", "no")
+
+
+def abl_id(c, m, s):
+    return 16 + 4 * ABL_C.index(c) + 2 * int(bool(m)) + int(bool(s))
+
+
+for _c in ABL_C:
+    for _m in (0, 1):
+        for _s in (0, 1):
+            HEURISTICS[f"abl_{_c}_{'m' if _m else 'x'}{'s' if _s else 'x'}"] = abl_id(_c, _m, _s)
 ENGINE_CTA, ENGINE_GRID = 1, 2
 DEALLOC = {"v2": 0, "v1": 1, "eager": 2, "ignore": 3}
 STATUS_NAMES = {0: "ok", 1: "inval", 2: "precond", 3: "oom", 4: "thrash_killed", 5: "capacity",

@@ -92,7 +92,7 @@ __device__ void init_sim(const Sim<SM> &g, const u32 *logw, u32 rank, u32 size, 
     g.crec(t) = make_uint2(0, 0);
     g.m.w(g.L.fr + t) = 0;                      // fill cursor (the stack is unused until the leader starts)
     if (heur == H_DTR) g.m.w(g.L.stamp + t) = 0;
-    if (heur == H_DTR_EQ) g.m.w(g.L.node_of + t) = NONE;
+    if (uses_uf(heur)) g.m.w(g.L.node_of + t) = NONE;
   }
   for (u32 j = rank; j < E; j += size) g.par(j) = lpar[j];
   for (u32 w = rank; w < g.L.pool_words; w += size) g.pool_word(w) = 0;
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(CTA_THREADS) percall_engine(PercallArgs a) {
       g.pool_pos(t) = NONE;
       g.crec(t) = make_uint2(NONE, 0);
       if (g.L.heur == H_DTR) g.m.w(g.L.stamp + t) = 0;
-      if (g.L.heur == H_DTR_EQ) g.m.w(g.L.node_of + t) = NONE;
+      if (uses_uf(g.L.heur)) g.m.w(g.L.node_of + t) = NONE;
     }
     if (uses_closure(g.L.heur)) {
       const u32 words = g.L.msps_words * g.L.msps_warps;
@@ -615,7 +615,7 @@ int dtr_batch_workspace_bytes(const uint32_t *dims, uint32_t n_cells, uint32_t e
   if (!bytes_out || (n_cells && !dims) || (engine != DTR_ENGINE_CTA && engine != DTR_ENGINE_GRID)) return DTR_E_INVAL;
   u64 cur = WS_HEADER, mx = 0;
   for (u32 i = 0; i < n_cells; i++) {
-    if (dims[3 * i + 2] > H_LAST) return DTR_E_INVAL;
+    if (!valid_heuristic(dims[3 * i + 2])) return DTR_E_INVAL;
     u64 b = cell_bytes(dims[3 * i], dims[3 * i + 1], dims[3 * i + 2], engine);
     if (engine == DTR_ENGINE_GRID) mx = b > mx ? b : mx;
     else cur += b;
@@ -723,7 +723,7 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
 }
 
 int dtr_pool_argmin(const uint32_t *d_log, uint32_t heuristic, void *d_ws, uint64_t *d_out, void *stream) {
-  if (!d_log || !d_ws || !d_out || heuristic > H_LAST) return DTR_E_INVAL;
+  if (!d_log || !d_ws || !d_out || !valid_heuristic(heuristic)) return DTR_E_INVAL;
   int dev, sms, per_sm = 0, blocks;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -830,7 +830,7 @@ static int rt_launch(dtr_runtime *rt, u32 init, u32 op_word) {
 }
 
 int dtr_create(const dtr_config *cfg, dtr_runtime **out) {
-  if (!cfg || !out || cfg->cap_tensors == 0 || cfg->heuristic > H_LAST || cfg->dealloc > DEALLOC_IGNORE)
+  if (!cfg || !out || cfg->cap_tensors == 0 || !valid_heuristic(cfg->heuristic) || cfg->dealloc > DEALLOC_IGNORE)
     return DTR_E_INVAL;
   if (cfg->cap_tensors >= (1u << 29)) return DTR_E_INVAL;
   dtr_runtime *rt = new dtr_runtime();

@@ -46,7 +46,18 @@ constexpr u64 CLOCK_LIMIT = 0xFFFFFFFEull;   // reading C-14: la is stored as cl
 
 enum { H_DTR = 0, H_DTR_EQ = 1, H_LRU = 2, H_SIZE = 3, H_MSPS = 4, H_LOCAL = 5, H_RANDOM = 6,
        H_DTR_FULL = 7, H_ESTAR = 8, H_LAST = 8 };
-__host__ __device__ __forceinline__ bool uses_closure(u32 h) { return h == H_MSPS || h == H_DTR_FULL || h == H_ESTAR; }
+// the D.1 ablation h'(s, m, c) (reading C-23): id = H_ABL + 4*c + 2*m + s,
+// c in {e*, EqClass, local, no}
+enum { H_ABL = 16, H_ABL_END = 32, ABL_ESTAR = 0, ABL_EQCLASS = 1, ABL_LOCAL = 2, ABL_NO = 3 };
+__host__ __device__ __forceinline__ bool is_abl(u32 h) { return h >= H_ABL && h < H_ABL_END; }
+__host__ __device__ __forceinline__ u32 abl_c(u32 h) { return (h - H_ABL) >> 2; }
+__host__ __device__ __forceinline__ bool valid_heuristic(u32 h) { return h <= H_LAST || is_abl(h); }
+// directed closures walked per candidate by one warp (MSPS, e*)
+__host__ __device__ __forceinline__ bool uses_closure(u32 h) {
+  return h == H_MSPS || h == H_DTR_FULL || h == H_ESTAR || (is_abl(h) && abl_c(h) == ABL_ESTAR);
+}
+// union-find evicted components
+__host__ __device__ __forceinline__ bool uses_uf(u32 h) { return h == H_DTR_EQ || (is_abl(h) && abl_c(h) == ABL_EQCLASS); }
 enum { OP_MAKE = 1, OP_GET = 2, OP_RELEASE = 3, OP_REMAT = 4, OP_ENSURE = 5, OP_DEBUG_EVICT = 6,
        OP_SCORES = 7 /* per-call only: score the whole pool */ };
 enum { DEALLOC_V2 = 0, DEALLOC_V1 = 1, DEALLOC_EAGER = 2, DEALLOC_IGNORE = 3 };
@@ -102,7 +113,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
     L.comp_head = take(n1);
     L.bfs_q = take(n1);
     L.stamp = take(n1);
-  } else if (heur == H_DTR_EQ) {
+  } else if (uses_uf(heur)) {
     L.uf_cap = n + 64;
     L.node_of = take(n1);
     L.uf = take(4 * (u64)L.uf_cap);

@@ -122,7 +122,7 @@ struct Leader {
       pool_remove(t);
     } else if (is_evicted(st)) {                     // leaves its evicted component
       if (s.heuristic == H_DTR) remat_exact(t, sr, st & COMP_MASK);
-      else if (s.heuristic == H_DTR_EQ) remat_uf(t, sr.y);
+      else if (uses_uf(s.heuristic)) remat_uf(t, sr.y);
     }
     auto pin = [&](u32 c) {                           // c.l := c.l + 1 (pinned: out of the pool)
       if (is_banished(g.state(c))) return;
@@ -302,7 +302,7 @@ struct Leader {
     if (s.heuristic == H_DTR) {
       u32 c = sp & COMP_MASK;
       if (v > g.comp(c).z) g.comp(c).z = v;
-    } else if (s.heuristic == H_DTR_EQ) {
+    } else if (uses_uf(s.heuristic)) {
       u32 r = uf_find(g.m.w(g.L.node_of + p));
       if (v > g.uf(r).z) g.uf(r).z = v;
     }
@@ -315,7 +315,7 @@ struct Leader {
     s.M -= sr.x;
     pool_remove(t);
     if (s.heuristic == H_DTR) evict_exact(t, sr, g.la(t));
-    else if (s.heuristic == H_DTR_EQ) evict_uf(t, sr, g.la(t));
+    else if (uses_uf(s.heuristic)) evict_uf(t, sr, g.la(t));
   }
 
   __device__ __forceinline__ void fnv(u64 v) { s.trace_hash = (s.trace_hash ^ v) * 1099511628211ull; }
@@ -370,7 +370,7 @@ struct Leader {
     if (st & O_BIT) {
       s.remats++;
       if (s.heuristic == H_DTR) remat_exact(t, sr, st & COMP_MASK);
-      else if (s.heuristic == H_DTR_EQ) remat_uf(t, sr.y);
+      else if (uses_uf(s.heuristic)) remat_uf(t, sr.y);
     } else if (g.L.linked) {
       // first computation: t becomes a visible child of its parents (reading C-19)
       for (u32 j = 0; j < sr.w; j++) {
@@ -451,7 +451,7 @@ struct Leader {
         g.rho(id) = 1;
         g.ell(id) = 0;
         if constexpr (!BM) g.pool_pos(id) = NONE;
-        if (s.heuristic == H_DTR_EQ) g.m.w(g.L.node_of + id) = NONE;
+        if (uses_uf(s.heuristic)) g.m.w(g.L.node_of + id) = NONE;
         if (g.L.linked) g.crec(id) = make_uint2(NONE, 0);
         for (u32 j = 0; j < sr.w; j++) {          // p.C u= {t}; p.last_accessed := clock
           u32 p = g.par(sr.z + j);

@@ -190,6 +190,14 @@ __device__ __forceinline__ Cand warp_argmin_fast(const Cand &c, u32 k) {
   return warp_argmin(below ? c : cand_none());
 }
 
+// h'(s, m, c) = c / (m * s) with ablated measures = 1 (reading C-23)
+__device__ __forceinline__ void abl_finish(u64 c, u32 mem, u32 la, const Cmd &cmd, Cand &out) {
+  const u32 code = cmd.heur - H_ABL;
+  const u32 m = (code & 2) ? mem : 1u;
+  if (code & 1) stale_score(c, m, la, cmd.clock, out.num, out.den);
+  else { out.num = c; out.den = m; }
+}
+
 // per-heuristic score of pool member t
 template <bool SM, int H>
 __device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t, Cand &c, u64 &bytes) {
@@ -211,6 +219,21 @@ __device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t,
     const uint4 sr = g.srec(t);
     stale_score((u64)sr.y, sr.x, g.la(t), cmd.clock, c.num, c.den);
     bytes += 12;
+  } else if constexpr (H == H_ABL) {           // h'(s, m, c) with c in {EqClass, local, no}
+    const uint4 sr = g.srec(t);
+    const u32 cc = abl_c(cmd.heur);
+    u64 num = 1;
+    if (cc == ABL_EQCLASS) {                   // c(t) + the distinct adjacent sets' costs
+      u64 sum = 0;
+      u32 L = 0;
+      nbr_components<SM, true>(g, t, sr, sum, L, bytes);
+      num = (u64)sr.y + sum;
+      bytes += 8;
+    } else if (cc == ABL_LOCAL) {
+      num = sr.y;
+    }
+    abl_finish(num, sr.x, g.la(t), cmd, c);
+    bytes += 16 + 4;
   } else {
     c.num = splitmix64(cmd.seed ^ (cmd.decisions << 32) ^ (u64)t); c.den = 1;
     bytes += 4;
@@ -349,7 +372,12 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
     case H_SIZE: score_loop<SM, BM, H_SIZE, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
     case H_LOCAL: score_loop<SM, BM, H_LOCAL, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
     case H_RANDOM: score_loop<SM, BM, H_RANDOM, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    default: break;
+    default:
+      if (is_abl(cmd.heur) && abl_c(cmd.heur) != ABL_ESTAR) {
+        score_loop<SM, BM, H_ABL, 2>(g, cmd, rank, size, best, bk, bytes, evals);
+        return best;
+      }
+      break;
   }
   // H_MSPS: one warp per candidate
   const u32 nw = wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
@@ -372,6 +400,9 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
         c.id = t;
         if (cmd.heur == H_DTR_FULL) {            // (c(S) + sum_{e*(S)} c) / (size(S) * stale(S))
           stale_score((u64)sr.y + sum, sr.x, g.la(t), cmd.clock, c.num, c.den);
+          bytes += 4;
+        } else if (is_abl(cmd.heur)) {           // h'(s, m, e*)
+          abl_finish((u64)sr.y + sum, sr.x, g.la(t), cmd, c);
           bytes += 4;
         } else {                                 // MSPS and h_e* (P:1835-1837): (c0 + sum) / m
           c.num = (u64)sr.y + sum;
@@ -403,6 +434,11 @@ __device__ void team_scores_out(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 
       if (lane == 0) {
         u64 num = (u64)sr.y + sum, den = sr.x;
         if (cmd.heur == H_DTR_FULL) stale_score((u64)sr.y + sum, sr.x, g.la(t), cmd.clock, num, den);
+        if (is_abl(cmd.heur)) {
+          Cand c;
+          abl_finish((u64)sr.y + sum, sr.x, g.la(t), cmd, c);
+          num = c.num; den = c.den;
+        }
         onum[i] = num; oden[i] = den; oid[i] = t;
       }
     }
@@ -417,7 +453,8 @@ __device__ void team_scores_out(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 
       case H_LRU: score_h<SM, H_LRU>(g, cmd, t, c, junk); break;
       case H_SIZE: score_h<SM, H_SIZE>(g, cmd, t, c, junk); break;
       case H_LOCAL: score_h<SM, H_LOCAL>(g, cmd, t, c, junk); break;
-      default: score_h<SM, H_RANDOM>(g, cmd, t, c, junk); break;
+      case H_RANDOM: score_h<SM, H_RANDOM>(g, cmd, t, c, junk); break;
+      default: score_h<SM, H_ABL>(g, cmd, t, c, junk); break;
     }
     onum[i] = c.num; oden[i] = c.den; oid[i] = t;
   }

@@ -40,7 +40,9 @@ def make_cells(log_views, permilles, heuristics, thrash_kill=16, max_decisions=0
 def est_cost(cell, log_views):
     v = log_views[cell["log"]]
     pm = max(int(cell.get("permille", 1000)), 50)
-    return v.n_ops * (1000.0 / pm) * HEUR_WEIGHT.get(cell["heuristic"], 1.0)
+    h = cell["heuristic"]
+    w = HEUR_WEIGHT.get(h, 8.0 if h in (16, 17, 18, 19) else 3.0 if h in (20, 21, 22, 23) else 1.0)
+    return v.n_ops * (1000.0 / pm) * w
 
 
 def shard(cells, log_views, world_size):

@@ -190,6 +190,69 @@ def test_percall_dealloc_random(P, oracle_mod):
                 assert g.trace().tobytes() == o.trace().tobytes()
 
 
+# ------------------------------------------------------------------ D.1 ablation h'(s, m, c) (reading C-23)
+
+ABL = [f"abl_{c}_{m}{s}" for c in ("estar", "eqclass", "local", "no") for m in "xm" for s in "xs"]
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_ablation_random(P, oracle_mod, engine):
+    logs, specs = [], []
+    for s in range(8 if engine == 1 else 2):
+        w = models.random_program(70, seed=4000 + s, p_release=0.3, max_parents=4)
+        logs.append(w)
+        v = LogView(w)
+        for fr in (0.35, 0.7):
+            for h in ABL:
+                specs.append(dict(log=len(logs) - 1, h=h, budget=max(3, int(v.peak_live * fr)),
+                                  dealloc="v1" if s % 2 else "v2"))
+    assert_parity(P, oracle_mod, logs, specs, engine)
+
+
+def test_ablation_models(P, oracle_mod):
+    """The 16 variants on resnet32 and unet (the paper's D.1 workloads are these logs)."""
+    logs = [models.resnet32(), models.unet()]
+    specs = []
+    for li, w in enumerate(logs):
+        v = LogView(w)
+        specs += [dict(log=li, h=h, budget=v.budget(pm)) for h in ABL for pm in (300, 700)]
+    assert_parity(P, oracle_mod, logs, specs, 1)
+
+
+def test_ablation_grid_and_pool_argmin(P, oracle_mod):
+    import torch
+    w = models.transformer()
+    v = LogView(w)
+    specs = [dict(log=0, h=h, budget=v.budget(400), max_decisions=300) for h in ABL]
+    assert_parity(P, oracle_mod, [w], specs, 2)
+    w = models.random_dag(100000, seed=12)
+    v = LogView(w)
+    for h in ("abl_estar_ms", "abl_eqclass_ms", "abl_eqclass_mx", "abl_local_xs", "abl_no_xx"):
+        D = 20
+        B = v.peak_total * 97 // 100
+        ref, tr = oracle_mod.replay(w, oracle_mod.HEURISTICS[h], B, max_decisions=D + 1, trace_cap=D + 1)
+        b = P.DeviceBatch([w], [dict(log=0, budget=B, heuristic=P.HEURISTICS[h], max_decisions=D)],
+                          engine=P.ENGINE_GRID)
+        b.run()
+        out = b.pool_argmin().cpu().numpy().astype(np.uint64)
+        torch.cuda.synchronize()
+        nxt = tr[D]
+        assert (int(out[0]), int(out[1]), int(out[2])) == (int(nxt["num"]), int(nxt["den"]), int(nxt["id"])), h
+
+
+def test_percall_ablation_fixture(P):
+    """Hand scores of tests/golden/ablation_T_B_clock7.json through the per-call API."""
+    import json, os
+    from fractions import Fraction
+    gd = os.path.join(os.path.dirname(__file__), "golden")
+    g = json.load(open(os.path.join(gd, "hdtr_T_B_clock7.json")))
+    a = json.load(open(os.path.join(gd, "ablation_T_B_clock7.json")))
+    for name, exp in a["expect"].items():
+        rt = percall_fixture(P, "abl_" + name, g["parents"], g["evict"])
+        got = {k: Fraction(n, d) for k, (n, d) in rt.scores().items()}
+        assert got == {int(k): Fraction(*v) for k, v in exp.items()}, name
+
+
 # ------------------------------------------------------------------ config 2 / 3
 
 def sweep_specs(v, hs, permilles, log=0, **kw):
