@@ -186,6 +186,45 @@ int dtr_replay_batch_host(const uint32_t *h_words, uint64_t n_words, const dtr_c
                           dtr_evict_rec *h_trace, uint64_t trace_total, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * The Theorem 2 adversary (App. B; reading C-24): one
+ * run per dtr_adversary, one CTA per run, all runs in one launch.  The graph is
+ * generated online from the runtime's residency: t0 (unit size and cost,
+ * locked resident by one ENSURE) gets B children t1..tB (the B paths); after
+ * that every node is the child of the last node of the lowest-indexed path with
+ * no resident node.  Unit sizes and costs; nothing is released.  The run stops
+ * after N nodes (t0 included) or at the first error (OOM cannot happen for
+ * B >= 3).  Static path-at-a-time cost is N.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  uint32_t n;              /* N >= 1: nodes to reveal, t0 included (< 2^27)            */
+  uint32_t budget;         /* B >= 3 memory units; t0 holds one          */
+  uint32_t heuristic;      /* dtr_heuristic                                             */
+  uint32_t cell_id;        /* copied to the result row                                  */
+  uint64_t seed;           /* DTR_H_RANDOM draws                                        */
+  uint64_t trace_offset;   /* first dtr_evict_rec of this run in d_trace                */
+  uint32_t trace_cap;      /* eviction records kept for this run (0 = none)             */
+  uint32_t reserved;       /* 0                                                         */
+} dtr_adversary;           /* 40 bytes */
+
+/* Device workspace for a batch of runs (h_runs on the HOST): 256 B plus one
+ * 256-B aligned region per run (used when a run's state does not fit in
+ * shared memory).  DTR_E_INVAL for n == 0, n >= 2^27, budget < 3 or an unknown
+ * heuristic. */
+int dtr_adversary_workspace_bytes(const dtr_adversary *h_runs, uint32_t n_runs, uint64_t *bytes);
+
+/* Run the batch asynchronously on `stream`.  d_runs: the runs in device memory,
+ * h_runs: the same array on the host (sizes the launch).  Outputs (device):
+ * d_rows[n_runs] result rows (clock = computations for unit costs; status DTR_OK
+ * when all N nodes were revealed); d_parents: for run i at offset sum_{k<i} n_k,
+ * parents[t] = the parent of node t (0xFFFFFFFF for t0 and for unrevealed
+ * nodes); d_trace: eviction records at each run's trace_offset (may be NULL when
+ * every trace_cap is 0).  Returns DTR_E_INVAL / DTR_E_CAPACITY (ws too small) /
+ * DTR_E_CUDA; per-run failures are reported in the rows. */
+int dtr_adversary_batch(const dtr_adversary *d_runs, const dtr_adversary *h_runs, uint32_t n_runs, void *d_ws,
+                        uint64_t ws_bytes, dtr_result *d_rows, uint32_t *d_parents, dtr_evict_rec *d_trace,
+                        void *stream);
+
+/* ---------------------------------------------------------------------------
  * Per-call runtime: the simrd external API, one call at a time.
  * The same device engine is fed one record per call; all state lives in
  * device memory owned by the runtime.  Calls are synchronous.

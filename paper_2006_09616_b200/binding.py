@@ -44,13 +44,17 @@ RESULT_DTYPE = np.dtype([("cell_id", "<u4"), ("status", "<u4"), ("records_done",
 CELL_DTYPE = np.dtype([("log_offset", "<u8"), ("budget", "<u8"), ("seed", "<u8"), ("max_decisions", "<u8"),
                        ("trace_offset", "<u8"), ("trace_cap", "<u8"), ("heuristic", "<u4"),
                        ("thrash_kill", "<u4"), ("cell_id", "<u4"), ("dealloc", "<u4")])
+ADV_DTYPE = np.dtype([("n", "<u4"), ("budget", "<u4"), ("heuristic", "<u4"), ("cell_id", "<u4"),
+                      ("seed", "<u8"), ("trace_offset", "<u8"), ("trace_cap", "<u4"), ("reserved", "<u4")])
 assert TRACE_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 88 and CELL_DTYPE.itemsize == 64
+assert ADV_DTYPE.itemsize == 40
 
 # every symbol include/dtr.h declares
 EXPORTS = ["dtr_strerror", "dtr_last_cuda_error", "dtr_version", "dtr_batch_workspace_bytes",
            "dtr_replay_batch", "dtr_replay_batch_host", "dtr_create", "dtr_destroy", "dtr_compute", "dtr_get",
            "dtr_release", "dtr_rematerialize", "dtr_ensure", "dtr_stats", "dtr_trace", "dtr_debug_evict",
-           "dtr_debug_set_budget", "dtr_debug_scores", "dtr_pool_argmin"]
+           "dtr_debug_set_budget", "dtr_debug_scores", "dtr_pool_argmin", "dtr_adversary_workspace_bytes",
+           "dtr_adversary_batch"]
 
 
 class DtrError(RuntimeError):
@@ -82,6 +86,10 @@ def _load():
     L.dtr_replay_batch.argtypes = [P, P, P, u32, u32, P, u64, P, P, P]
     L.dtr_pool_argmin.restype = i32
     L.dtr_pool_argmin.argtypes = [P, u32, P, P, P]
+    L.dtr_adversary_workspace_bytes.restype = i32
+    L.dtr_adversary_workspace_bytes.argtypes = [P, u32, C.POINTER(u64)]
+    L.dtr_adversary_batch.restype = i32
+    L.dtr_adversary_batch.argtypes = [P, P, u32, P, u64, P, P, P, P]
     L.dtr_replay_batch_host.restype = i32
     L.dtr_replay_batch_host.argtypes = [P, u64, P, u32, u32, P, P, u64, P]
     L.dtr_create.restype = i32
@@ -245,6 +253,65 @@ class DeviceBatch:
         tr = self.traces() if tr is None else tr
         c = self.h_cells[i]
         return tr[int(c["trace_offset"]): int(c["trace_offset"]) + int(c["trace_cap"])]
+
+
+# ---------------------------------------------------------------------------
+# Theorem 2 adversary batches (App. B; include/dtr.h dtr_adversary_batch)
+# ---------------------------------------------------------------------------
+
+class AdversaryBatch:
+    """Runs of the online adversary, one CTA each, one launch per run() call.
+    runs: dicts {n, budget, heuristic, seed=0, trace_cap=0, cell_id=i}."""
+
+    def __init__(self, runs, device=None):
+        import torch
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        a = np.zeros(len(runs), dtype=ADV_DTYPE)
+        toff = 0
+        for i, r in enumerate(runs):
+            a[i]["n"] = int(r["n"])
+            a[i]["budget"] = int(r["budget"])
+            a[i]["heuristic"] = int(r["heuristic"])
+            a[i]["cell_id"] = int(r.get("cell_id", i))
+            a[i]["seed"] = int(r.get("seed", 0))
+            a[i]["trace_cap"] = int(r.get("trace_cap", 0))
+            a[i]["trace_offset"] = toff
+            toff += int(a[i]["trace_cap"])
+        self.h_runs = a
+        self.n_runs = len(runs)
+        self.p_off = np.concatenate([[0], np.cumsum(a["n"].astype(np.int64))])
+        nb = C.c_uint64(0)
+        _check(lib.dtr_adversary_workspace_bytes(_np_ptr(a), len(a), C.byref(nb)), "dtr_adversary_workspace_bytes")
+        dev = self.device
+        self.ws_bytes = int(nb.value)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.d_runs = torch.from_numpy(a.view(np.uint8).copy()).to(dev)
+        self.rows = torch.zeros(len(a) * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        self.parents = torch.zeros(int(self.p_off[-1]), dtype=torch.int32, device=dev)
+        self.trace_total = toff
+        self.trace = torch.zeros(max(toff, 1) * TRACE_DTYPE.itemsize, dtype=torch.uint8, device=dev) if toff else None
+
+    def run(self, stream=None):
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        _check(lib.dtr_adversary_batch(self.d_runs.data_ptr(), _np_ptr(self.h_runs), self.n_runs, self.ws.data_ptr(),
+                                       self.ws_bytes, self.rows.data_ptr(), self.parents.data_ptr(),
+                                       self.trace.data_ptr() if self.trace is not None else None, s.cuda_stream),
+               "dtr_adversary_batch")
+
+    def result_rows(self):
+        return self.rows.cpu().numpy().view(RESULT_DTYPE).copy()
+
+    def run_parents(self, i, all_parents=None):
+        p = self.parents.cpu().numpy().view(np.uint32) if all_parents is None else all_parents
+        return p[int(self.p_off[i]): int(self.p_off[i + 1])].copy()
+
+    def run_trace(self, i):
+        if self.trace is None:
+            return None
+        tr = self.trace.cpu().numpy().view(TRACE_DTYPE)
+        o, c = int(self.h_runs[i]["trace_offset"]), int(self.h_runs[i]["trace_cap"])
+        return tr[o: o + c].copy()
 
 
 # ---------------------------------------------------------------------------

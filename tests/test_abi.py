@@ -57,3 +57,44 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("oracle/ (shares no code", ""), f
+
+
+def test_header_struct_layouts_match_the_binding(tmp_path):
+    """sizeof / offsetof of every struct in include/dtr.h (compiled by gcc) equal
+    the numpy dtypes the binding marshals."""
+    import subprocess
+    import paper_2006_09616_b200 as P
+    structs = {"dtr_cell": P.CELL_DTYPE, "dtr_result": P.RESULT_DTYPE, "dtr_evict_rec": P.TRACE_DTYPE,
+               "dtr_adversary": P.ADV_DTYPE}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dtr.h"', "int main(void) {"]
+    for s, dt in structs.items():
+        lines.append(f'  printf("{s} sizeof %zu\\n", sizeof({s}));')
+        for f in dt.names:
+            lines.append(f'  printf("{s} {f} %zu\\n", offsetof({s}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = subprocess.check_output([str(exe)]).decode().split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l}
+    for s, dt in structs.items():
+        assert got[(s, "sizeof")] == dt.itemsize, s
+        for f in dt.names:
+            assert got[(s, f)] == dt.fields[f][1], (s, f)
+
+
+def test_adversary_workspace_validation():
+    import pytest
+    import paper_2006_09616_b200 as P
+    b = np.zeros(2, dtype=P.ADV_DTYPE)
+    b["n"] = 100
+    b["budget"] = 8
+    b["heuristic"] = [8, 21]
+    import ctypes as C
+    nb = C.c_uint64(0)
+    assert P.lib.dtr_adversary_workspace_bytes(C.c_void_p(b.ctypes.data), 2, C.byref(nb)) == 0 and nb.value > 256
+    for field, bad in (("budget", 2), ("n", 0), ("heuristic", 9)):
+        c = b.copy()
+        c[field][0] = bad
+        assert P.lib.dtr_adversary_workspace_bytes(C.c_void_p(c.ctypes.data), 2, C.byref(nb)) == 1   # DTR_E_INVAL
