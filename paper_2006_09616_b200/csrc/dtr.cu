@@ -36,7 +36,8 @@ using namespace dtr;
 #define WS_BSTATS 98816      /* per-block {bytes, evals} for dtr_pool_argmin */
 #define WS_SCALARS 128       /* grid engine: final Scalars of the last cell */
 #define WS_PARTIALS 512
-#define CTA_SMEM_MAX (200u * 1024u)
+#define WS_SLOWN 124         /* whole-GPU team: slow-queue length (u32) */
+#define CTA_SMEM_MAX (225u * 1024u)  /* + ~1 KB static CtaShared <= 227 KB per block */
 
 // ---------------------------------------------------------------------------
 // Initialisation (team-parallel): static records and parents from the log,
@@ -86,10 +87,10 @@ __device__ void init_sim(const Sim<SM> &g, const u32 *logw, u32 rank, u32 size, 
   const u32 *lmem = logw + 16, *lcost = lmem + n, *loff = lcost + n, *lpar = loff + n + 1;
   for (u32 t = rank; t < n; t += size) {
     const u32 b = loff[t], e = loff[t + 1];
-    g.srec(t) = make_uint4(lmem[t], lcost[t], b, e - b);
-    g.state(t) = 0; g.la(t) = 0; g.rho(t) = 0; g.ell(t) = 0;
+    g.srec(t) = make_uint4(lmem[t], lcost[t], 0, 0);     // la = -inf, nev = 0
+    g.arec(t) = make_uint4(b, e - b, 0, 0);               // children counted below
+    g.state(t) = 0; g.rho(t) = 0; g.ell(t) = 0;
     g.pool_pos(t) = NONE;
-    g.crec(t) = make_uint2(0, 0);
     g.m.w(g.L.fr + t) = 0;                      // fill cursor (the stack is unused until the leader starts)
     if (heur == H_DTR) g.m.w(g.L.stamp + t) = 0;
     if (uses_uf(heur)) g.m.w(g.L.node_of + t) = NONE;
@@ -187,7 +188,8 @@ __device__ __forceinline__ void leader_init(Leader<SM, BM> &L, const Sim<SM> &g,
 // ---------------------------------------------------------------------------
 __host__ __device__ inline u64 cell_bytes(u32 n, u32 E, u32 heur, u32 engine) {
   Lay L;
-  make_layout(L, n, E, heur, 0, engine == DTR_ENGINE_GRID ? GRID_MSPS_WARPS : CTA_THREADS / 32);
+  make_layout(L, n, E, heur, 0, engine == DTR_ENGINE_GRID ? GRID_MSPS_WARPS : CTA_THREADS / 32,
+              engine == DTR_ENGINE_GRID);
   return ((u64)L.words * 4 + 255) & ~255ull;
 }
 
@@ -272,7 +274,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
         u32 bk;
         Cand best = team_score<SM, false>(g, c, lane, 32, 0, 1, sh.msps_tail, bytes, evals, bk);
         PROF_T(t3);
-        best = warp_argmin_fast(best, bk);
+        best = warp_argmin_fast(best, bk, int_key_heur(c.heur));
         PROF_T(t4);
         if (lane == 0) { res = best; have = true; PROF_ADD(1, t3 - t2); PROF_ADD(2, t4 - t3); PROF_ADD(3, 1); }
         continue;
@@ -283,7 +285,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       if (c.kind != CMD_ARGMIN) break;
       u32 bk;
       Cand best = team_score<SM, false>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk);
-      best = block_argmin(best, bk, sh.red);
+      best = block_argmin(best, bk, sh.red, int_key_heur(c.heur));
       PROF_T(t6);
       if (lane == 0) { res = best; have = true; PROF_ADD(4, t6 - t5); PROF_ADD(5, 1); }
     }
@@ -295,7 +297,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       if (c.kind != CMD_ARGMIN) break;
       u32 bk;
       Cand best = team_score<SM, false>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk);
-      block_argmin(best, bk, sh.red);
+      block_argmin(best, bk, sh.red, int_key_heur(c.heur));
     }
   }
   block_sum2(bytes, evals, sh.red);
@@ -372,10 +374,11 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
   }
   Sim<false> g;
   g.m.gbase = (u32 *)(ws + WS_HEADER);
-  make_layout(g.L, logw[2], logw[3], cell.heuristic, 0, GRID_MSPS_WARPS);
+  make_layout(g.L, logw[2], logw[3], cell.heuristic, 0, GRID_MSPS_WARPS, 1);
   const u32 rank = blockIdx.x * blockDim.x + tid, size = gridDim.x * blockDim.x;
   const u32 wrank = rank >> 5, wsize = size >> 5;
-  if (rank == 0) { gstats[0] = 0; gstats[1] = 0; *(u32 *)(ws + 120) = 0; }
+  u32 *slown = (u32 *)(ws + WS_SLOWN);
+  if (rank == 0) { gstats[0] = 0; gstats[1] = 0; *slown = 0; }
   init_sim(g, logw, rank, size, blockIdx.x == 0, sh.scan, GridSync());
   Leader<false, true> L;
   if (rank == 0) leader_init(L, g, logw, cell, trace);
@@ -391,6 +394,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
       Cmd c;
       publish(c, kind, L.s);
       *gcmd = c;
+      *slown = 0;                   // every warp has finished reading it (grid barrier since)
       PROF_T(a1);
       PROF_ADD(0, a1 - a0);
     }
@@ -409,23 +413,25 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
     if (sh.cmd.kind != CMD_ARGMIN) break;
     u32 bk;
     PROF_T(c0);
-    Cand best = team_score<false, true, true>(g, sh.cmd, rank, size, wrank, wsize, sh.msps_tail, bytes, evals, bk);
+    Cand best = team_score<false, true, true>(g, sh.cmd, rank, size, wrank, wsize, sh.msps_tail, bytes, evals, bk,
+                                              slown);
     PROF_T(c1);
-    best = block_argmin(best, bk, sh.red);
+    const bool ik = int_key_heur(sh.cmd.heur);
+    best = block_argmin(best, bk, sh.red, ik);
     if (tid == 0) partials[blockIdx.x] = best;
     PROF_T(c2);
     grid.sync();
     PROF_T(c3);
     if (rank == 0) { PROF_ADD(2, c1 - c0); PROF_ADD(3, c2 - c1); PROF_ADD(4, c3 - c2); PROF_ADD(5, 1); }
-    if (blockIdx.x == 0 && tid < 32) {
+    if (blockIdx.x == 0) {          // block 0 reduces the per-block partials (one load per thread)
       Cand c = cand_none();
       u32 ck = KEY_NONE;
-      for (u32 b = tid; b < gridDim.x; b += 32) {
+      for (u32 b = tid; b < gridDim.x; b += blockDim.x) {
         Cand d;
         d.num = __ldcg(&partials[b].num); d.den = __ldcg(&partials[b].den); d.id = __ldcg(&partials[b].id);
-        cand_take(c, ck, d);
+        cand_take(c, ck, d, ik);
       }
-      c = warp_argmin_fast(c, ck);
+      c = block_argmin(c, ck, sh.red, ik);
       if (tid == 0) { res = c; have = true; }
     }
   }
@@ -451,16 +457,15 @@ struct __align__(16) PaShared {
   u32 msps_tail[PA_THREADS / 32];
 };
 
-__global__ void __launch_bounds__(PA_THREADS, 2) pool_argmin_kernel(const u32 *logw, u32 heur, char *ws,
+__global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *logw, u32 heur, char *ws,
                                                                     u64 *out /* num, den, id, bytes, evals */) {
   __shared__ PaShared sh;
-  __shared__ bool last;
   const u32 tid = threadIdx.x;
   Cand *partials = (Cand *)(ws + WS_PARTIALS);
-  u32 *arrive = (u32 *)(ws + 120);
+  u32 *slown = (u32 *)(ws + WS_SLOWN);
   Sim<false> g;
   g.m.gbase = (u32 *)(ws + WS_HEADER);
-  make_layout(g.L, logw[2], logw[3], heur, 0, GRID_MSPS_WARPS);
+  make_layout(g.L, logw[2], logw[3], heur, 0, GRID_MSPS_WARPS, 1);
   const Scalars *sc = (const Scalars *)(ws + WS_SCALARS);
   Cmd cmd;
   cmd.kind = CMD_ARGMIN; cmd.pool_size = sc->pool_size; cmd.clock = sc->clock; cmd.decisions = sc->decisions;
@@ -468,34 +473,33 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pool_argmin_kernel(const u32 *l
   const u32 rank = blockIdx.x * blockDim.x + tid, size = gridDim.x * blockDim.x;
   u64 bytes = 0, evals = 0;
   u32 bk;
-  Cand best = team_score<false, true, true>(g, cmd, rank, size, rank >> 5, size >> 5, sh.msps_tail, bytes, evals, bk);
-  best = block_argmin(best, bk, sh.red);
+  Cand best = team_score<false, true, true>(g, cmd, rank, size, rank >> 5, size >> 5, sh.msps_tail, bytes, evals, bk,
+                                            slown);
+  const bool ik = int_key_heur(heur);
+  best = block_argmin(best, bk, sh.red, ik);
   block_sum2(bytes, evals, sh.red);
   u64 *bstats = (u64 *)(ws + WS_BSTATS);
   if (tid == 0) {
     partials[blockIdx.x] = best;
     bstats[2 * blockIdx.x] = bytes;
     bstats[2 * blockIdx.x + 1] = evals;
-    __threadfence();
-    last = atomicAdd(arrive, 1u) == gridDim.x - 1;
   }
-  __syncthreads();
-  if (last && tid < 32) {
-    __threadfence();
+  cg::this_grid().sync();
+  if (blockIdx.x == 0) {      // block 0 reduces the partials (all loads in flight)
     Cand c = cand_none();
     u32 ck = KEY_NONE;
     u64 tb = 0, te = 0;
-    for (u32 b = tid; b < gridDim.x; b += 32) {
+    for (u32 b = tid; b < gridDim.x; b += blockDim.x) {
       Cand d;
       d.num = __ldcg(&partials[b].num); d.den = __ldcg(&partials[b].den); d.id = __ldcg(&partials[b].id);
-      cand_take(c, ck, d);
+      cand_take(c, ck, d, ik);
       tb += __ldcg(&bstats[2 * b]);
       te += __ldcg(&bstats[2 * b + 1]);
     }
-    c = warp_argmin_fast(c, ck);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) { tb += __shfl_xor_sync(0xffffffffu, tb, o); te += __shfl_xor_sync(0xffffffffu, te, o); }
-    if (tid == 0) { out[0] = c.num; out[1] = c.den; out[2] = c.id; out[3] = tb; out[4] = te; *arrive = 0; }
+    c = block_argmin(c, ck, sh.red, ik);
+    Cand w = c;
+    block_sum2(tb, te, sh.red);
+    if (tid == 0) { out[0] = w.num; out[1] = w.den; out[2] = w.id; out[3] = tb; out[4] = te; *slown = 0; }
   }
 }
 
@@ -523,7 +527,8 @@ __global__ void __launch_bounds__(CTA_THREADS) percall_engine(PercallArgs a) {
   if (a.init) {
     for (u32 w = tid; w < g.L.pool_words; w += blockDim.x) g.pool_word(w) = 0;
     for (u32 t = tid; t <= g.L.n; t += blockDim.x) {
-      g.state(t) = 0; g.la(t) = 0; g.rho(t) = 0; g.ell(t) = 0;
+      g.srec(t) = make_uint4(0, 0, 0, 0);
+      g.state(t) = 0; g.rho(t) = 0; g.ell(t) = 0;
       g.pool_pos(t) = NONE;
       g.crec(t) = make_uint2(NONE, 0);
       if (g.L.heur == H_DTR) g.m.w(g.L.stamp + t) = 0;
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(CTA_THREADS) percall_engine(PercallArgs a) {
     u32 bk;
     Cand best = team_score<false, false>(g, sh.cmd, tid, blockDim.x, tid >> 5, blockDim.x >> 5, sh.msps_tail, junk, junk2,
                                          bk);
-    best = block_argmin(best, bk, sh.red);
+    best = block_argmin(best, bk, sh.red, int_key_heur(sh.cmd.heur));
     if (tid == 0) { res = best; have = true; }
   }
   if (tid == 0) *a.sc = L.s;
@@ -628,7 +633,7 @@ __device__ void adv_apply(Leader<SM, false> &L, const Sim<SM> &g, AdvShared &sh,
     u32 bk;
     Cand best = team_score<SM, false>(g, sh.cmd, tid, blockDim.x, tid >> 5, blockDim.x >> 5, sh.msps_tail, bytes,
                                       evals, bk);
-    best = block_argmin(best, bk, sh.red);
+    best = block_argmin(best, bk, sh.red, int_key_heur(sh.cmd.heur));
     if (tid == 0) { res = best; have = true; }
   }
   __syncthreads();
@@ -645,7 +650,8 @@ __device__ void run_adversary(const dtr_adversary &run, u32 *gbase, dtr_result *
   adv_layout(g.L, A, N, B, run.heuristic);
   for (u32 w = tid; w < g.L.pool_words; w += blockDim.x) g.pool_word(w) = 0;
   for (u32 t = tid; t <= N; t += blockDim.x) {
-    g.state(t) = 0; g.la(t) = 0; g.rho(t) = 0; g.ell(t) = 0;
+    g.srec(t) = make_uint4(0, 0, 0, 0);
+    g.state(t) = 0; g.rho(t) = 0; g.ell(t) = 0;
     g.pool_pos(t) = NONE;
     g.crec(t) = make_uint2(NONE, 0);
     if (g.L.heur == H_DTR) g.m.w(g.L.stamp + t) = 0;
@@ -699,7 +705,8 @@ __device__ void run_adversary(const dtr_adversary &run, u32 *gbase, dtr_result *
       const u32 t = L.s.n_alloc;
       u32 p = NONE, j = NONE;
       if (nx == ADV_T0) {
-        g.srec(0) = make_uint4(1, 1, edges, 0);
+        g.srec(0) = make_uint4(1, 1, 0, 0);
+        g.prec(0) = make_uint2(edges, 0);
       } else if (nx == ADV_CHILD || nx == ADV_SCAN) {
         if (nx == ADV_CHILD) {
           j = t - 1;
@@ -714,7 +721,8 @@ __device__ void run_adversary(const dtr_adversary &run, u32 *gbase, dtr_result *
         }
         if (j != NONE) {
           p = nx == ADV_CHILD ? 0u : g.m.w(A.tail + j);
-          g.srec(t) = make_uint4(1, 1, edges, 1);
+          g.srec(t) = make_uint4(1, 1, 0, 0);
+          g.prec(t) = make_uint2(edges, 1);
           g.par(edges) = p;
         }
       }
@@ -864,12 +872,16 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
   char *ws = (char *)d_ws;
   if (engine == DTR_ENGINE_CTA) {
     // Consecutive cells of the same shared-memory class form one launch: small
-    // (<= 48 KiB: several CTAs per SM), large (<= 200 KiB staged), global (state
+    // (<= 48 KiB: several CTAs per SM), large (<= 225 KiB staged), global (state
     // stays in the workspace).  Classes run concurrently on forked streams.
     static cudaStream_t cls_st[3];
     static cudaEvent_t fork_ev, join_ev[3];
     static bool init = false;
+    static int sm_count = 0;
     if (!init) {
+      int dev;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
       CK(cudaFuncSetAttribute(cta_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTA_SMEM_MAX));
       for (int k = 0; k < 3; k++) {
         CK(cudaStreamCreateWithFlags(&cls_st[k], cudaStreamNonBlocking));
@@ -901,6 +913,9 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
         if (c != 2 && nd > smem) smem = nd;
       }
       smem = (smem + 15) & ~15ull;
+      // at most one cell per SM: reserve more than half an SM's shared memory so
+      // no two CTAs (each a latency-bound single-leader simulation) share an SM
+      if (c != 2 && n_cells <= (u32)sm_count && !getenv("DTR_PACK_CTAS")) smem = std::max<u64>(smem, 116u * 1024u);
       cudaStream_t ls = st;
       if (!single) {
         ls = cls_st[c];
@@ -942,8 +957,8 @@ int dtr_pool_argmin(const uint32_t *d_log, uint32_t heuristic, void *d_ws, uint6
   blocks = sms * (per_sm < 1 ? 1 : per_sm);
   if (blocks > 4096) blocks = 4096;
   cudaStream_t st = (cudaStream_t)stream;
-  pool_argmin_kernel<<<blocks, PA_THREADS, 0, st>>>(d_log, heuristic, (char *)d_ws, (u64 *)d_out);
-  CK(cudaGetLastError());
+  void *args[] = {(void *)&d_log, (void *)&heuristic, (void *)&d_ws, (void *)&d_out};
+  CK(cudaLaunchCooperativeKernel((void *)pool_argmin_kernel, dim3(blocks), dim3(PA_THREADS), args, 0, st));
   return DTR_OK;
 }
 
@@ -1150,8 +1165,10 @@ int dtr_compute(dtr_runtime *rt, uint32_t mem, uint32_t compute, const uint32_t 
   }
   if (t >= rt->cfg.cap_tensors) return DTR_E_CAPACITY;
   if ((u64)rt->edges + ps.size() > rt->cfg.cap_edges) return DTR_E_CAPACITY;
-  uint4 sr = make_uint4(mem, compute, rt->edges, (u32)ps.size());
+  const uint4 sr = make_uint4(mem, compute, 0, 0);            // {mem, cost, la, nev}
+  const uint2 pr = make_uint2(rt->edges, (u32)ps.size());     // {par_off, npar}
   CK(cudaMemcpyAsync(rt->d_ws + rt->L.srec + 4 * (u64)t, &sr, 16, cudaMemcpyHostToDevice, rt->st));
+  CK(cudaMemcpyAsync(rt->d_ws + rt->L.arec + 4 * (u64)t, &pr, 8, cudaMemcpyHostToDevice, rt->st));
   if (!ps.empty())
     CK(cudaMemcpyAsync(rt->d_ws + rt->L.par + rt->edges, ps.data(), 4 * ps.size(), cudaMemcpyHostToDevice, rt->st));
   int rc = rt_launch(rt, 0, (OP_MAKE << 29) | t);

@@ -12,9 +12,12 @@
 // Memory: every array of a simulation is addressed by a 32-bit WORD offset from
 // one base -- the CTA's dynamic shared memory (SM = true: LDS/STS, 32-bit
 // addresses) or the simulation's global workspace (SM = false).
-//   srec[t] = {mem, cost, par_off, npar}          (static, from the log; one 16-B load)
-//   crec[t] = {ch_off, nch}  | linked: {head, -}  (children, built on device)
-//   state[t], la[t], rho[t], ell[t]               (dynamic, compact u32 arrays: a
+//   srec[t] = {mem, cost, la, nev}                 the score record: mem and cost
+//             static (from the log), la and nev dynamic -- everything a
+//             candidate with no evicted neighbour needs, in one 16-B load
+//   arec[t] = {par_off, npar, ch_off, nch}         adjacency record; the children
+//             half (crec) is built on device | linked: {head, -}
+//   state[t], rho[t], ell[t]                      (dynamic, compact u32 arrays: a
 //             neighbour's state word shares its sector with nearby ids)
 //   pool     R.pool (t.m = T and t.l = 0), one of two representations:
 //            - compact list pool_ids[] + pool_pos[] (CTA engine, per-call): the
@@ -25,6 +28,10 @@
 //   state: bit31 material (t.m = T), bit30 computed once (reading C-19),
 //          bit29 V1-banished, bits 0..28 label of t's evicted component (h_DTR)
 //   la:    last_access + 1, 0 = -inf (banish_V2)
+//   nev:   number of t's neighbours (parents, children) that are evicted --
+//          maintained by the leader on evict / rematerialize / V1 banish for the
+//          heuristics that read neighbourhoods (Lay.track_nev); nev = 0 means
+//          E(t) = e*(t) = e_R(t) = {} and the score needs no neighbour walk
 //
 // Independent of oracle/ (shares no code with it).
 #pragma once
@@ -72,29 +79,30 @@ __host__ __device__ __forceinline__ bool is_material(u32 s) { return (s & M_BIT)
 // Layout: word offsets of every array of one simulation.
 // ---------------------------------------------------------------------------
 struct Lay {
-  u32 n, E, heur, linked;
-  u32 srec, crec, par, ch, state, la, rho, ell, pool_bm, pool_words, pool_ids, pool_pos, fr, pb;
+  u32 n, E, heur, linked, track_nev;
+  u32 srec, arec, par, ch, state, rho, ell, pool_bm, pool_words, pool_ids, pool_pos, fr, pb;
   u32 mem_next, comp, comp_head, bfs_q, stamp;         // h_DTR (comp rec: {cost lo, cost hi, maxla, size})
   u32 node_of, uf, uf_size, uf_cap;                    // h_DTR_eq (uf rec: {cost lo, cost hi, maxla, parent})
   u32 msps_bm, msps_q, msps_words, msps_warps;         // h_MSPS per-warp scratch
   u32 e_next, e_child;                                 // linked children (per-call)
+  u32 slowq;                                           // whole-GPU team: candidates with nev > 0
   u32 words;                                           // total
-  u32 pad;
 };
 
 // Sizes the workspace (host) and places it (device).  Returns false when the
 // layout does not fit 32-bit word offsets.
-__host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 linked, u32 msps_warps) {
+__host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 linked, u32 msps_warps,
+                                            u32 grid = 0) {
   u64 o = 0;
   auto take = [&](u64 words) -> u32 { u64 p = o; o = (o + words + 3) & ~3ull; return (u32)p; };
   const u64 n1 = (u64)n + 1, e1 = (u64)E + 1;
   L.n = n; L.E = E; L.heur = heur; L.linked = linked;
+  L.track_nev = heur == H_DTR || uses_uf(heur) || uses_closure(heur);
   L.srec = take(4 * n1);
-  L.crec = take(2 * n1);
+  L.arec = take(4 * n1);
   L.par = take(e1);
   L.ch = linked ? 0 : take(e1);
   L.state = take(n1);
-  L.la = take(n1);
   L.rho = take(n1);
   L.ell = take(n1);
   L.pool_words = (u32)((n1 + 31) / 32);
@@ -128,8 +136,8 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
     L.e_next = take(e1);
     L.e_child = take(e1);
   }
+  L.slowq = grid ? take(n1) : 0;
   L.words = (u32)o;
-  L.pad = 0;
   return o < 0xFFFFFFF0ull;
 }
 
@@ -245,10 +253,13 @@ struct Sim {
   Mem<SM> m;
   Lay L;
 
-  __device__ __forceinline__ uint4 &srec(u32 t) const { return m.q(L.srec + 4 * t); }
-  __device__ __forceinline__ uint2 &crec(u32 t) const { return m.d(L.crec + 2 * t); }
+  __device__ __forceinline__ uint4 &srec(u32 t) const { return m.q(L.srec + 4 * t); }     // {mem, cost, la, nev}
+  __device__ __forceinline__ u32 &la(u32 t) const { return m.w(L.srec + 4 * t + 2); }
+  __device__ __forceinline__ u32 &nev(u32 t) const { return m.w(L.srec + 4 * t + 3); }
+  __device__ __forceinline__ uint4 &arec(u32 t) const { return m.q(L.arec + 4 * t); }     // {par_off, npar, ch_off, nch}
+  __device__ __forceinline__ uint2 &prec(u32 t) const { return m.d(L.arec + 4 * t); }     // {par_off, npar}
+  __device__ __forceinline__ uint2 &crec(u32 t) const { return m.d(L.arec + 4 * t + 2); } // {ch_off, nch} | {head, -}
   __device__ __forceinline__ u32 &state(u32 t) const { return m.w(L.state + t); }
-  __device__ __forceinline__ u32 &la(u32 t) const { return m.w(L.la + t); }
   __device__ __forceinline__ u32 &rho(u32 t) const { return m.w(L.rho + t); }
   __device__ __forceinline__ u32 &ell(u32 t) const { return m.w(L.ell + t); }
   __device__ __forceinline__ u32 &par(u32 j) const { return m.w(L.par + j); }
@@ -259,15 +270,15 @@ struct Sim {
   __device__ __forceinline__ uint4 &comp(u32 c) const { return m.q(L.comp + 4 * c); }
   __device__ __forceinline__ uint4 &uf(u32 x) const { return m.q(L.uf + 4 * x); }
 
-  // parents of t (srec already loaded) then children
+  // parents of t then children (ar = arec(t) already loaded; linked lists are
+  // re-read from the live head)
   template <class F>
-  __device__ __forceinline__ void for_each_nbr(u32 t, const uint4 &sr, F f) const {
-    for (u32 j = 0; j < sr.w; j++) f(par(sr.z + j));
-    uint2 cr = crec(t);
+  __device__ __forceinline__ void for_each_nbr(u32 t, const uint4 &ar, F f) const {
+    for (u32 j = 0; j < ar.y; j++) f(par(ar.x + j));
     if (!L.linked) {
-      for (u32 j = 0; j < cr.y; j++) f(m.w(L.ch + cr.x + j));
+      for (u32 j = 0; j < ar.w; j++) f(m.w(L.ch + ar.z + j));
     } else {
-      for (u32 e = cr.x; e != NONE; e = m.w(L.e_next + e)) f(m.w(L.e_child + e));
+      for (u32 e = crec(t).x; e != NONE; e = m.w(L.e_next + e)) f(m.w(L.e_child + e));
     }
   }
 

@@ -88,7 +88,7 @@ struct Leader {
 
   // ------------------------------------------------------------- V1 banishing (reading C-22)
   // children of t that exist (created), are not banished, and are not material?
-  __device__ bool child_not_material(u32 t) {
+  __device__ __forceinline__ bool child_not_material(u32 t) {
     const uint2 cr = g.crec(t);
     bool bad = false;
     if (!g.L.linked) {
@@ -105,23 +105,25 @@ struct Leader {
       }
       // the tensor under creation is already in t.C but not yet linked
       if (!bad && s.n_alloc > 0 && !(g.state(s.n_alloc - 1) & O_BIT)) {
-        const uint4 sn = g.srec(s.n_alloc - 1);
-        for (u32 j = 0; j < sn.w; j++) if (g.par(sn.z + j) == t) bad = true;
+        const uint2 pn = g.prec(s.n_alloc - 1);
+        for (u32 j = 0; j < pn.y; j++) if (g.par(pn.x + j) == t) bad = true;
       }
     }
     return bad;
   }
-  __device__ void maybe_banish(u32 t) {
+  __device__ __forceinline__ void maybe_banish(u32 t) {
     const u32 st = g.state(t);
     if (is_banished(st) || g.rho(t) != 0 || child_not_material(t)) return;
     // banish_V1
     const uint4 sr = g.srec(t);
+    const uint4 ar = g.arec(t);
     g.state(t) = (st & O_BIT) | B_BIT;
     if (is_material(st)) {
       s.M -= sr.x;
       pool_remove(t);
     } else if (is_evicted(st)) {                     // leaves its evicted component
-      if (s.heuristic == H_DTR) remat_exact(t, sr, st & COMP_MASK);
+      nev_add(t, ar, NONE);
+      if (s.heuristic == H_DTR) remat_exact(t, ar, st & COMP_MASK);
       else if (uses_uf(s.heuristic)) remat_uf(t, sr.y);
     }
     auto pin = [&](u32 c) {                           // c.l := c.l + 1 (pinned: out of the pool)
@@ -136,6 +138,16 @@ struct Leader {
     } else {
       for (u32 e = cr.x; e != NONE; e = g.m.w(g.L.e_next + e)) pin(g.m.w(g.L.e_child + e));
     }
+  }
+
+  // ------------------------------------------------------------- evicted-neighbour counts
+  // t has just become evicted (d = 1) or stopped being evicted (d = -1): every
+  // neighbour's nev changes by d.  Tensors not yet created may be counted too;
+  // every such count is back to 0 by their first computation (all parents are
+  // resident then), where it is reset anyway for the linked (per-call) lists.
+  __device__ __forceinline__ void nev_add(u32 t, const uint4 &ar, u32 d) {
+    if (!g.L.track_nev) return;
+    g.for_each_nbr(t, ar, [&](u32 q) { g.nev(q) += d; });
   }
 
   // ------------------------------------------------------------- exact components
@@ -153,13 +165,15 @@ struct Leader {
   }
 
   // t has just become evicted: {t} joins the components of its evicted neighbours.
-  __device__ __forceinline__ void evict_exact(u32 t, const uint4 &sr, u32 la) {
-    g.comp(t) = make_uint4(sr.y, 0, la, 1);
+  // (fused: every neighbour's nev += 1)
+  __device__ __forceinline__ void evict_exact(u32 t, const uint4 &sr, const uint4 &ar) {
+    g.comp(t) = make_uint4(sr.y, 0, sr.z, 1);
     g.m.w(g.L.comp_head + t) = t;
     g.m.w(g.L.mem_next + t) = NONE;
     g.state(t) = O_BIT | t;
     u32 cur = t;
-    g.for_each_nbr(t, sr, [&](u32 q) {
+    g.for_each_nbr(t, ar, [&](u32 q) {
+      g.nev(q) += 1;
       u32 sq = g.state(q);
       if (!is_evicted(sq)) return;
       u32 cq = sq & COMP_MASK;
@@ -170,10 +184,10 @@ struct Leader {
   // t (formerly in component c) has just become material: relabel c \ {t} by
   // BFS from t's evicted neighbours; each BFS tree becomes a component labelled
   // by its root (a member).
-  __device__ __forceinline__ void remat_exact(u32 t, const uint4 &sr, u32 c) {
+  __device__ __forceinline__ void remat_exact(u32 t, const uint4 &ar, u32 c) {
     if (g.comp(c).w == 1) return;
     u32 ep = ++s.epoch;
-    g.for_each_nbr(t, sr, [&](u32 q) {
+    g.for_each_nbr(t, ar, [&](u32 q) {
       u32 sq = g.state(q);
       if (!is_evicted(sq) || g.m.w(g.L.stamp + q) == ep) return;
       u32 head = 0, tail = 0;
@@ -183,15 +197,15 @@ struct Leader {
       u32 mx = 0, list = NONE, size = 0;
       while (head < tail) {
         u32 x = g.m.w(g.L.bfs_q + head++);
-        uint4 sx = g.srec(x);
+        const uint4 sx = g.srec(x);
+        const uint4 ax = g.arec(x);
         g.state(x) = O_BIT | q;
         g.m.w(g.L.mem_next + x) = list;
         list = x;
         size++;
         cost += sx.y;
-        u32 lx = g.la(x);
-        mx = lx > mx ? lx : mx;
-        g.for_each_nbr(x, sx, [&](u32 y) {
+        mx = sx.z > mx ? sx.z : mx;
+        g.for_each_nbr(x, ax, [&](u32 y) {
           if (is_evicted(g.state(y)) && g.m.w(g.L.stamp + y) != ep) {
             g.m.w(g.L.stamp + y) = ep;
             g.m.w(g.L.bfs_q + tail++) = y;
@@ -242,7 +256,7 @@ struct Leader {
   // node array is full, renumber the live roots in place, in increasing old id
   // (new id <= old id, so no live record is overwritten before it moves): the
   // sets, their cost and maxla -- all the heuristic reads -- are unchanged.
-  __device__ void uf_compact() {
+  __device__ __forceinline__ void uf_compact() {
     const u32 SZ = g.L.uf_size;
     for (u32 q = 0; q < s.n_alloc; q++) {              // point every evicted tensor at its root
       if (!is_evicted(g.state(q))) continue;
@@ -278,12 +292,14 @@ struct Leader {
   }
   // "When a tensor t is evicted, its component is unioned with those of any
   // evicted neighbors and c0(t) is added to the component's running sum"
-  __device__ __forceinline__ void evict_uf(u32 t, const uint4 &sr, u32 la) {
+  // (fused: every neighbour's nev += 1)
+  __device__ __forceinline__ void evict_uf(u32 t, const uint4 &sr, const uint4 &ar) {
     u32 n0 = uf_alloc();
-    g.uf(n0) = make_uint4(sr.y, 0, la, n0);
+    g.uf(n0) = make_uint4(sr.y, 0, sr.z, n0);
     g.m.w(g.L.uf_size + n0) = 1;
     g.m.w(g.L.node_of + t) = n0;
-    g.for_each_nbr(t, sr, [&](u32 q) {
+    g.for_each_nbr(t, ar, [&](u32 q) {
+      g.nev(q) += 1;
       if (is_evicted(g.state(q))) uf_union(n0, g.m.w(g.L.node_of + q));
     });
   }
@@ -310,12 +326,14 @@ struct Leader {
 
   // ------------------------------------------------------------- evict
   __device__ __forceinline__ void evict(u32 t) {
-    uint4 sr = g.srec(t);
+    const uint4 sr = g.srec(t);
+    const uint4 ar = g.arec(t);
     g.state(t) = O_BIT;
     s.M -= sr.x;
     pool_remove(t);
-    if (s.heuristic == H_DTR) evict_exact(t, sr, g.la(t));
-    else if (uses_uf(s.heuristic)) evict_uf(t, sr, g.la(t));
+    if (s.heuristic == H_DTR) evict_exact(t, sr, ar);
+    else if (uses_uf(s.heuristic)) evict_uf(t, sr, ar);
+    else nev_add(t, ar, 1u);
   }
 
   __device__ __forceinline__ void fnv(u64 v) { s.trace_hash = (s.trace_hash ^ v) * 1099511628211ull; }
@@ -334,10 +352,10 @@ struct Leader {
 
   // ------------------------------------------------------------- get_internal stack
   // frame k: fr[k] = {t, pb_base, pb_count, next}
-  __device__ __forceinline__ void push(u32 t, const uint4 &sr) {
+  __device__ __forceinline__ void push(u32 t, const uint2 &pr) {
     u32 base = s.pb_top;
-    for (u32 j = 0; j < sr.w; j++) {           // P_T locked now, P_B kept in order (reading C-6)
-      u32 p = g.par(sr.z + j);
+    for (u32 j = 0; j < pr.y; j++) {           // P_T locked now, P_B kept in order (reading C-6)
+      u32 p = g.par(pr.x + j);
       if (is_material(g.state(p))) lock(p);
       else g.m.w(g.L.pb + s.pb_top++) = p;
     }
@@ -346,7 +364,7 @@ struct Leader {
   }
   __device__ __forceinline__ void start_gi(u32 t) {
     if (is_material(g.state(t))) lock(t);
-    else push(t, g.srec(t));
+    else push(t, g.prec(t));
   }
 
   __device__ __forceinline__ u32 stop(u32 st) {
@@ -359,7 +377,8 @@ struct Leader {
   // compute the top frame's tensor (its parents are all resident and locked,
   // and M + mem <= B): lines 234-240 of get_internal. Returns false on stop.
   __device__ __forceinline__ bool complete_top(u32 t, const uint4 &fr) {
-    uint4 sr = g.srec(t);
+    const uint4 sr = g.srec(t);
+    const uint4 ar = g.arec(t);
     u32 st = g.state(t);
     g.state(t) = M_BIT | O_BIT;
     g.ell(t) = 1;
@@ -369,21 +388,26 @@ struct Leader {
     s.computations++;
     if (st & O_BIT) {
       s.remats++;
-      if (s.heuristic == H_DTR) remat_exact(t, sr, st & COMP_MASK);
+      nev_add(t, ar, NONE);
+      if (s.heuristic == H_DTR) remat_exact(t, ar, st & COMP_MASK);
       else if (uses_uf(s.heuristic)) remat_uf(t, sr.y);
-    } else if (g.L.linked) {
-      // first computation: t becomes a visible child of its parents (reading C-19)
-      for (u32 j = 0; j < sr.w; j++) {
-        u32 p = g.par(sr.z + j);
-        u32 x = s.edges_used++;
-        g.m.w(g.L.e_child + x) = t;
-        g.m.w(g.L.e_next + x) = g.crec(p).x;
-        g.crec(p).x = x;
+    } else {
+      // first computation: every parent is resident and no child exists yet
+      if (g.L.track_nev) g.nev(t) = 0;
+      if (g.L.linked) {
+        // t becomes a visible child of its parents (reading C-19)
+        for (u32 j = 0; j < ar.y; j++) {
+          u32 p = g.par(ar.x + j);
+          u32 x = s.edges_used++;
+          g.m.w(g.L.e_child + x) = t;
+          g.m.w(g.L.e_next + x) = g.crec(p).x;
+          g.crec(p).x = x;
+        }
       }
     }
     if (s.clock > CLOCK_LIMIT) { stop(ST_CAPACITY); return false; }
     if (s.kill_limit && s.clock > s.kill_limit) { stop(ST_THRASH); return false; }
-    for (u32 j = 0; j < sr.w; j++) release_internal(g.par(sr.z + j));
+    for (u32 j = 0; j < ar.y; j++) release_internal(g.par(ar.x + j));
     s.pb_top = fr.y;
     s.sp--;
     return true;
@@ -405,7 +429,7 @@ struct Leader {
   }
 
   // ------------------------------------------------------------- the state machine
-  __device__ u32 resume(bool have, const Cand &res) {
+  __device__ __forceinline__ u32 resume(bool have, const Cand &res) {
     if (phase == PH_FREE && have) record_and_evict(res);
     if (phase == PH_SCORED) { finish_op(); phase = PH_OP; }
     for (;;) {
@@ -417,7 +441,7 @@ struct Leader {
           g.m.w(g.L.fr + 4 * k + 3) = fr.w + 1;
           u32 p = g.m.w(g.L.pb + fr.y + fr.w);
           if (is_material(g.state(p))) lock(p);
-          else push(p, g.srec(p));
+          else push(p, g.prec(p));
           continue;
         }
         u32 t = fr.x;
@@ -439,11 +463,12 @@ struct Leader {
       const u32 op = word >> 29, id = word & ((1u << 29) - 1);
       if (op == OP_MAKE) {
         if (id != s.n_alloc || id >= g.L.n) { if (!precond()) return CMD_DONE; continue; }
-        const uint4 sr = g.srec(id);
+        const u32 cost = g.srec(id).y;
+        const uint2 pr = g.prec(id);
         bool ok = true;
-        for (u32 j = 0; j < sr.w; j++) if (g.rho(g.par(sr.z + j)) == 0) ok = false;   // reading C-12
+        for (u32 j = 0; j < pr.y; j++) if (g.rho(g.par(pr.x + j)) == 0) ok = false;   // reading C-12
         if (!ok) { if (!precond()) return CMD_DONE; continue; }
-        s.base_so_far += sr.y;
+        s.base_so_far += cost;
         s.kill_limit = (u64)s.thrash_kill * s.base_so_far;
         const u32 now = (u32)(s.clock + 1);
         g.state(id) = 0;
@@ -453,15 +478,15 @@ struct Leader {
         if constexpr (!BM) g.pool_pos(id) = NONE;
         if (uses_uf(s.heuristic)) g.m.w(g.L.node_of + id) = NONE;
         if (g.L.linked) g.crec(id) = make_uint2(NONE, 0);
-        for (u32 j = 0; j < sr.w; j++) {          // p.C u= {t}; p.last_accessed := clock
-          u32 p = g.par(sr.z + j);
+        for (u32 j = 0; j < pr.y; j++) {          // p.C u= {t}; p.last_accessed := clock
+          u32 p = g.par(pr.x + j);
           g.la(p) = now;
           u32 sp = g.state(p);
           if (is_evicted(sp)) raise_maxla(p, sp, now);
         }
         s.n_alloc++;
         root = id; post = 1;
-        push(id, sr);
+        push(id, pr);
         phase = PH_GI;
         continue;
       }

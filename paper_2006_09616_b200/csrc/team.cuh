@@ -10,22 +10,29 @@
 //   h_MSPS    (c0(t) + sum_{e_R(t)} c0) / m(t)
 //   h_local   c0(t) / (m(t) s(t))
 //   h_random  splitmix64(seed ^ decision << 32 ^ t)                        P:1269 (C-15)
+// A candidate whose evicted-neighbour count nev is 0 has E(t) = e*(t) = e_R(t)
+// = {} and is scored from its 16-B score record {mem, cost, la, nev} alone;
+// only candidates with nev > 0 walk their neighbour lists.
 // Algorithmic bytes are counted as they are read: the
-// pool bitmap (1 bit per tensor id), per candidate its own fields (h_DTR: srec
-// 16 + la 4 + children record 8; LRU la 4; size mem 4; local 12; random 4),
-// then 8 per neighbour (id + state word), 12 per distinct component (cost +
-// max la), h_DTR_eq +4 per evicted neighbour (node id) and +4 per union-find
-// step; MSPS +8 per parent examined, +16 per closure member.
+// pool bitmap (1 bit per tensor id), per candidate its own fields (h_DTR,
+// h_DTR_eq, closures: score record 16; LRU la 4; size mem 4; local 12; random
+// 4), and when nev > 0: the adjacency record 16, then 8 per neighbour (id +
+// state word), 12 per distinct component (cost + max la), h_DTR_eq +4 per
+// evicted neighbour (node id) and +4 per union-find step; MSPS +8 per parent
+// examined, +16 per closure member.
 #pragma once
 #include "engine.cuh"
 #include "leader.cuh"
+#include <cooperative_groups.h>
 
 namespace dtr {
+
+namespace cg = cooperative_groups;
 
 // Distinct adjacent evicted components: the last four labels are kept in
 // registers; beyond four an earlier-neighbour rescan decides duplicates.
 template <bool SM, bool UF>
-__device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const uint4 &sr, u64 &sum, u32 &L,
+__device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const uint4 &ar, u64 &sum, u32 &L,
                                                u64 &bytes) {
   u32 c0 = NONE, c1 = NONE, c2 = NONE, c3 = NONE, nd = 0, nb = 0, extra = 0;
   auto comp_of = [&](u32 q, u32 sq, u32 &steps) -> u32 {
@@ -33,7 +40,7 @@ __device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const ui
     else return sq & COMP_MASK;
   };
   u32 pos = 0;
-  g.for_each_nbr(t, sr, [&](u32 q) {
+  g.for_each_nbr(t, ar, [&](u32 q) {
     const u32 my = pos++;
     nb++;
     const u32 sq = g.state(q);
@@ -45,7 +52,7 @@ __device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const ui
     if (nd >= 4) {
       u32 p2 = 0;
       bool dup = false;
-      g.for_each_nbr(t, sr, [&](u32 y) {
+      g.for_each_nbr(t, ar, [&](u32 y) {
         if (dup || p2 >= my) { p2++; return; }
         p2++;
         u32 sy = g.state(y), st2 = 0;
@@ -69,7 +76,7 @@ __device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const ui
 // so one per-warp visited bitmap + queue serves both passes; the sum of their
 // c0 is returned in every lane.
 template <bool SM>
-__device__ u64 msps_closure(const Sim<SM> &g, const uint4 &sr, u32 wslot, volatile u32 *tail, u64 &bytes,
+__device__ u64 msps_closure(const Sim<SM> &g, const uint4 &ar, u32 wslot, volatile u32 *tail, u64 &bytes,
                             u32 t = NONE, bool down = false) {
   const u32 lane = threadIdx.x & 31;
   const u32 bm = g.L.msps_bm + wslot * g.L.msps_words;
@@ -83,20 +90,20 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &sr, u32 wslot, volati
     u32 bit = 1u << (p & 31);
     u32 old = atomicOr(&g.m.w(bm + (p >> 5)), bit);
     if (old & bit) return;
-    bytes += 16;  // its static record
+    bytes += 16;  // its score record
     sum += g.srec(p).y;
     u32 pos = atomicAdd((u32 *)tail, 1u);
     g.m.w(q + pos) = p;
   };
-  for (u32 j = lane; j < sr.w; j += 32) visit(g.par(sr.z + j));
+  for (u32 j = lane; j < ar.y; j += 32) visit(g.par(ar.x + j));
   __syncwarp();
   u32 head = 0, tl = *tail;
   __syncwarp();
   while (head < tl) {
     for (u32 i = head + lane; i < tl; i += 32) {
       u32 x = g.m.w(q + i);
-      const uint4 sx = g.srec(x);
-      for (u32 j = 0; j < sx.w; j++) visit(g.par(sx.z + j));
+      const uint2 px = g.prec(x);
+      for (u32 j = 0; j < px.y; j++) visit(g.par(px.x + j));
     }
     __syncwarp();
     head = tl;
@@ -139,20 +146,27 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &sr, u32 wslot, volati
 // ---------------------------------------------------------------------------
 constexpr u32 KEY_NONE = 0xFFFFFFFFu, KEY_INF = 0x7F800000u, KEY_MARGIN = 256u;   // 256 ulps >= 2^-16 relative
 
-__device__ __forceinline__ u32 cand_key(const Cand &c) {
+// Integer keys (ik): h_size and h_LRU scores are 1/m and 1/s with integer m, s,
+// so key = ~den orders them exactly (score 0 -> 0, +inf -> 0xFFFFFFFE); equal
+// keys are still resolved exactly, so the margin is 0 and no division is done.
+__host__ __device__ __forceinline__ bool int_key_heur(u32 h) { return h == H_SIZE || h == H_LRU; }
+
+__device__ __forceinline__ u32 cand_key(const Cand &c, bool ik = false) {
   if (c.id == NONE) return KEY_NONE;
-  if (c.den == 0) return KEY_INF;
   if (c.num == 0) return 0u;
+  if (ik) return c.den == 0 ? 0xFFFFFFFEu : ~(u32)c.den;
+  if (c.den == 0) return KEY_INF;
   return __float_as_uint(__fdividef(__ull2float_rn(c.num), __ull2float_rn(c.den)));
 }
 
 // best := min(best, c) exactly; bk tracks key(best)
-__device__ __forceinline__ void cand_take(Cand &best, u32 &bk, const Cand &c) {
-  const u32 k = cand_key(c);
+__device__ __forceinline__ void cand_take(Cand &best, u32 &bk, const Cand &c, bool ik = false) {
+  const u32 k = cand_key(c, ik);
   if (k == KEY_NONE) return;
+  const u32 mg = ik ? 0u : KEY_MARGIN;
   bool better;
-  if (k + KEY_MARGIN < bk) better = true;
-  else if (bk != KEY_NONE && k > bk + KEY_MARGIN) better = false;
+  if (k + mg < bk) better = true;
+  else if (bk != KEY_NONE && k > bk + mg) better = false;
   else better = cand_less(c, best);
   if (better) { best = c; bk = k; }
 }
@@ -168,16 +182,16 @@ __device__ __forceinline__ Cand shfl_cand(const Cand &c, int src) {
 __device__ __forceinline__ Cand warp_argmin(Cand c);   // exact (below)
 
 // warp-wide exact argmin using the key fast path; every lane gets the result.
-__device__ __forceinline__ Cand warp_argmin_fast(const Cand &c, u32 k) {
+__device__ __forceinline__ Cand warp_argmin_fast(const Cand &c, u32 k, bool ik = false) {
   const u32 FULL = 0xffffffffu;
   const u32 kmin = __reduce_min_sync(FULL, k);
   if (kmin == KEY_NONE) return cand_none();
-  if (kmin == 0u || kmin == KEY_INF) {             // exact class: smallest id wins
+  if (kmin == 0u || (!ik && kmin == KEY_INF)) {    // exact class: smallest id wins
     const u32 idmin = __reduce_min_sync(FULL, k == kmin ? c.id : NONE);
     const u32 m = __ballot_sync(FULL, k == kmin && c.id == idmin);
     return shfl_cand(c, __ffs(m) - 1);
   }
-  const bool in = k <= kmin + KEY_MARGIN;
+  const bool in = k <= kmin + (ik ? 0u : KEY_MARGIN);
   const u32 cont = __ballot_sync(FULL, in);
   if (__popc(cont) == 1) return shfl_cand(c, __ffs(cont) - 1);
   // near-ties: take the contender with the smallest id as reference; if no
@@ -205,10 +219,13 @@ __device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t,
   if constexpr (H == H_DTR || H == H_DTR_EQ) {
     const uint4 sr = g.srec(t);
     u64 sum = 0;
-    u32 L = g.la(t);
-    nbr_components<SM, H == H_DTR_EQ>(g, t, sr, sum, L, bytes);
+    u32 L = sr.z;
+    bytes += 16;                  // score record
+    if (sr.w) {                   // evicted neighbours: walk them
+      nbr_components<SM, H == H_DTR_EQ>(g, t, g.arec(t), sum, L, bytes);
+      bytes += 16;                // adjacency record
+    }
     stale_score((u64)sr.y + sum, sr.x, L, cmd.clock, c.num, c.den);
-    bytes += 16 + 4 + 8;          // srec, la, crec
   } else if constexpr (H == H_LRU) {
     stale_score(1, 1, g.la(t), cmd.clock, c.num, c.den);
     bytes += 4;
@@ -217,7 +234,7 @@ __device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t,
     bytes += 4;
   } else if constexpr (H == H_LOCAL) {
     const uint4 sr = g.srec(t);
-    stale_score((u64)sr.y, sr.x, g.la(t), cmd.clock, c.num, c.den);
+    stale_score((u64)sr.y, sr.x, sr.z, cmd.clock, c.num, c.den);
     bytes += 12;
   } else if constexpr (H == H_ABL) {           // h'(s, m, c) with c in {EqClass, local, no}
     const uint4 sr = g.srec(t);
@@ -226,132 +243,267 @@ __device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t,
     if (cc == ABL_EQCLASS) {                   // c(t) + the distinct adjacent sets' costs
       u64 sum = 0;
       u32 L = 0;
-      nbr_components<SM, true>(g, t, sr, sum, L, bytes);
+      if (sr.w) {
+        nbr_components<SM, true>(g, t, g.arec(t), sum, L, bytes);
+        bytes += 16;
+      }
       num = (u64)sr.y + sum;
-      bytes += 8;
     } else if (cc == ABL_LOCAL) {
       num = sr.y;
     }
-    abl_finish(num, sr.x, g.la(t), cmd, c);
-    bytes += 16 + 4;
+    abl_finish(num, sr.x, sr.z, cmd, c);
+    bytes += 16;
   } else {
     c.num = splitmix64(cmd.seed ^ (cmd.decisions << 32) ^ (u64)t); c.den = 1;
     bytes += 4;
   }
 }
 
-// Whole-GPU h_DTR / h_DTR_eq for two candidates at once, in fixed unrolled
-// phases so every load of a phase is independent (in-order issue would
-// otherwise pay one memory latency per neighbour): own records -> all
-// neighbour ids -> all neighbour states (-> UF nodes) -> distinct component
-// records.  Candidates with more than NB neighbours use score_h.
+// One candidate with evicted neighbours per lane (whole-GPU team, phase 2), in
+// fixed unrolled phases so every load of a phase is independent (in-order
+// issue would otherwise pay one memory latency per neighbour): neighbour ids
+// -> their states (-> union-find roots) -> distinct component records.  Only
+// for deg(t) <= NB; returns the sum of the distinct adjacent components' cost
+// and the max of their max la with la(t).
 constexpr u32 NB = 8;
 
 template <bool UF>
-__device__ __forceinline__ void score_pair_dtr(const Sim<false> &g, const Cmd &cmd, const u32 *t, u32 k, Cand *c,
-                                               u64 &bytes) {
-  uint4 sr[2];
-  uint2 cr[2];
-  u32 la[2], deg[2];
+__device__ __forceinline__ void nbr_components_phased(const Sim<false> &g, const uint4 &sr, const uint4 &ar,
+                                                      u64 &sum, u32 &L, u64 &bytes) {
+  const u32 deg = ar.y + ar.w;
+  u32 q[NB], lab[NB];
 #pragma unroll
-  for (u32 a = 0; a < 2; a++) {
-    if (a < k) { sr[a] = g.srec(t[a]); cr[a] = g.crec(t[a]); la[a] = g.la(t[a]); }
-    else { sr[a] = make_uint4(0, 0, 0, 0); cr[a] = make_uint2(0, 0); la[a] = 0; }
-    deg[a] = sr[a].w + cr[a].y;
+  for (u32 j = 0; j < NB; j++)
+    q[j] = j < deg ? (j < ar.y ? g.par(ar.x + j) : g.m.w(g.L.ch + ar.z + (j - ar.y))) : NONE;
+#pragma unroll
+  for (u32 j = 0; j < NB; j++) lab[j] = q[j] != NONE ? g.state(q[j]) : 0;
+#pragma unroll
+  for (u32 j = 0; j < NB; j++) {
+    const u32 sq = lab[j];
+    if constexpr (UF) lab[j] = is_evicted(sq) ? g.m.w(g.L.node_of + q[j]) : NONE;
+    else lab[j] = is_evicted(sq) ? (sq & COMP_MASK) : NONE;
   }
-  u32 q[2][NB];
-#pragma unroll
-  for (u32 a = 0; a < 2; a++)
-#pragma unroll
-    for (u32 j = 0; j < NB; j++)
-      q[a][j] = (a < k && deg[a] <= NB && j < deg[a])
-                    ? (j < sr[a].w ? g.par(sr[a].z + j) : g.m.w(g.L.ch + cr[a].x + (j - sr[a].w))) : NONE;
-  u32 lab[2][NB];
-#pragma unroll
-  for (u32 a = 0; a < 2; a++)
-#pragma unroll
-    for (u32 j = 0; j < NB; j++) lab[a][j] = q[a][j] != NONE ? g.state(q[a][j]) : 0;
-#pragma unroll
-  for (u32 a = 0; a < 2; a++)
-#pragma unroll
-    for (u32 j = 0; j < NB; j++) {
-      const u32 sq = lab[a][j];
-      if constexpr (UF) lab[a][j] = is_evicted(sq) ? g.m.w(g.L.node_of + q[a][j]) : NONE;
-      else lab[a][j] = is_evicted(sq) ? (sq & COMP_MASK) : NONE;
-    }
   if constexpr (UF) {
     u32 steps = 0;
 #pragma unroll
-    for (u32 a = 0; a < 2; a++)
-#pragma unroll
-      for (u32 j = 0; j < NB; j++)
-        if (lab[a][j] != NONE) { lab[a][j] = g.uf_root(lab[a][j], steps); bytes += 4; }
+    for (u32 j = 0; j < NB; j++)
+      if (lab[j] != NONE) { lab[j] = g.uf_root(lab[j], steps); bytes += 4; }
     bytes += 4ull * steps;
   }
+  u32 cc[NB], cl[NB], ch[NB], nd = 0;
 #pragma unroll
-  for (u32 a = 0; a < 2; a++) {
-    if (a >= k) continue;
-    if (deg[a] > NB) { score_h<false, UF ? H_DTR_EQ : H_DTR>(g, cmd, t[a], c[a], bytes); continue; }
-    u64 sum = 0;
-    u32 L = la[a], nd = 0;
-    u32 cc[NB], cl[NB], ch[NB];
+  for (u32 j = 0; j < NB; j++) {
+    bool first = lab[j] != NONE;
 #pragma unroll
-    for (u32 j = 0; j < NB; j++) {
-      bool first = lab[a][j] != NONE;
+    for (u32 i = 0; i < j; i++) first = first && lab[i] != lab[j];
+    ch[j] = first ? lab[j] : NONE;
+  }
 #pragma unroll
-      for (u32 i = 0; i < j; i++) first = first && lab[a][i] != lab[a][j];
-      ch[j] = first ? lab[a][j] : NONE;
+  for (u32 j = 0; j < NB; j++) {            // distinct component records, all in flight
+    if (ch[j] != NONE) {
+      const uint4 r = UF ? g.uf(ch[j]) : g.comp(ch[j]);
+      cc[j] = r.x; cl[j] = r.z; ch[j] = r.y;   // ch reused: cost high word
+      nd++;
+    } else {
+      cc[j] = 0; cl[j] = 0; ch[j] = 0;
     }
+  }
+  u64 s = 0;
+  u32 mx = sr.z;
 #pragma unroll
-    for (u32 j = 0; j < NB; j++) {          // distinct component records, all in flight
-      if (ch[j] != NONE) {
-        const uint4 r = UF ? g.uf(ch[j]) : g.comp(ch[j]);
-        cc[j] = r.x; cl[j] = r.z; ch[j] = r.y;   // ch reused: cost high word
-      }
+  for (u32 j = 0; j < NB; j++) { s += mk64(cc[j], ch[j]); mx = cl[j] > mx ? cl[j] : mx; }
+  sum = s;
+  L = mx;
+  bytes += 16 + 8ull * deg + 12ull * nd;     // adjacency record, ids + states, components
+}
+
+// Warp-cooperative E(t) aggregation for ONE candidate t with evicted neighbours
+// (whole-GPU team, phase 2): lane j takes neighbour j (chunks of 32), so the
+// chain adjacency record -> neighbour ids -> states (-> union-find roots) ->
+// distinct component records costs four round trips whatever the degree.
+// Duplicate labels are dropped with __match_any_sync within a chunk and by a
+// shuffle scan against earlier chunks (degree > 32 only).  All lanes return
+// the sum of the distinct adjacent components' cost and the max of their max
+// la with la(t) (sr.z); bytes are counted per lane.
+template <bool UF>
+__device__ __forceinline__ void nbr_components_warp(const Sim<false> &g, u32 t, const uint4 &sr, u64 &sum, u32 &L,
+                                                    u64 &bytes) {
+  const u32 FULL = 0xffffffffu, lane = threadIdx.x & 31;
+  const uint4 ar = g.arec(t);
+  const u32 deg = ar.y + ar.w;
+  auto label = [&](u32 j, u64 &b) -> u32 {
+    if (j >= deg) return NONE;
+    const u32 q = j < ar.y ? g.par(ar.x + j) : g.m.w(g.L.ch + ar.z + (j - ar.y));
+    const u32 sq = g.state(q);
+    b += 8;
+    if (!is_evicted(sq)) return NONE;
+    if constexpr (UF) {
+      u32 steps = 0;
+      const u32 r = g.uf_root(g.m.w(g.L.node_of + q), steps);
+      b += 4 + 4ull * steps;
+      return r;
+    } else {
+      return sq & COMP_MASK;
     }
-#pragma unroll
-    for (u32 j = 0; j < NB; j++) {
-      bool first = lab[a][j] != NONE;
-#pragma unroll
-      for (u32 i = 0; i < j; i++) first = first && lab[a][i] != lab[a][j];
-      if (first) { sum += mk64(cc[j], ch[j]); L = cl[j] > L ? cl[j] : L; nd++; }
+  };
+  u64 s = 0;
+  u32 mx = 0;
+  if (lane == 0) bytes += 16;                       // adjacency record
+  for (u32 base = 0; base < deg; base += 32) {
+    const u32 lab = label(base + lane, bytes);
+    const u32 grp = __match_any_sync(FULL, lab);
+    bool first = lab != NONE && (u32)(__ffs(grp) - 1) == lane;
+    for (u32 b0 = 0; b0 < base; b0 += 32) {         // earlier chunks (degree > 32)
+      u64 junk = 0;
+      const u32 prev = label(b0 + lane, junk);
+      for (u32 k = 0; k < 32; k++) first = first && __shfl_sync(FULL, prev, k) != lab;
     }
-    c[a].id = t[a];
-    stale_score((u64)sr[a].y + sum, sr[a].x, L, cmd.clock, c[a].num, c[a].den);
-    bytes += 16 + 4 + 8 + 8ull * deg[a] + 12ull * nd;
+    if (first) {
+      const uint4 r = UF ? g.uf(lab) : g.comp(lab);
+      s += mk64(r.x, r.y);
+      mx = r.z > mx ? r.z : mx;
+      bytes += 12;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(FULL, s, o);
+    const u32 m2 = __shfl_xor_sync(FULL, mx, o);
+    mx = m2 > mx ? m2 : mx;
+  }
+  sum = s;
+  L = mx > sr.z ? mx : sr.z;
+}
+
+// Score this thread's share of the compact pool list (CTA engine, per-call),
+// K candidates at a time (independent chains in flight), into best: the
+// members pool_ids[rank + j * size].
+template <bool SM, int H, u32 K>
+__device__ __forceinline__ void score_loop(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, Cand &best,
+                                           u32 &bk, u64 &bytes, u64 &evals) {
+  const u32 n = cmd.pool_size;
+  for (u32 i = rank; i < n; i += K * size) {
+    u32 cand[K];
+#pragma unroll
+    for (u32 r = 0; r < K; r++) cand[r] = i + r * size < n ? g.pool_ids(i + r * size) : NONE;
+    Cand c[K];
+#pragma unroll
+    for (u32 r = 0; r < K; r++)
+      if (cand[r] != NONE) { score_h<SM, H>(g, cmd, cand[r], c[r], bytes); bytes += 4; evals++; }
+#pragma unroll
+    for (u32 r = 0; r < K; r++)
+      if (cand[r] != NONE) cand_take(best, bk, c[r], int_key_heur(H));
   }
 }
 
-// Score this thread's share of the pool, K candidates at a time (independent
-// chains in flight), into best.  BM: scan tensor ids rank, rank + size, ... <
-// n_ids and take the pool members (bitmap); else take pool_ids[rank + j*size].
-template <bool SM, bool BM, int H, u32 K>
-__device__ __forceinline__ void score_loop(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, Cand &best,
-                                           u32 &bk, u64 &bytes, u64 &evals) {
-  const u32 n = BM ? cmd.n_ids : cmd.pool_size;
-  u32 i = rank;
-  while (i < n) {
-    u32 cand[K];
-    u32 k = 0;
-    while (k < K && i < n) {
-      if constexpr (BM) { if (g.in_pool(i)) cand[k++] = i; }
-      else { cand[k++] = g.pool_ids(i); bytes += 4; }
-      i += size;
+// Whole-GPU pass over the pool BITMAP (grid engine, dtr_pool_argmin; every
+// thread of a cooperative grid).  Phase 1: warp w takes bitmap words w, w + W,
+// w + 2W, ... (W = warps in the grid) and lane l the id 32 * word + l, so each
+// step reads one broadcast bitmap word and 32 consecutive score records (512 B,
+// coalesced), U steps in flight per lane; a candidate with nev = 0 is scored
+// from its record alone, one with evicted neighbours is appended to the slow
+// queue (one atomic per warp step).  Phase 2 (after a grid barrier): the slow
+// candidates are spread evenly over the grid, one per lane, so no warp
+// serialises a cluster of them; a candidate of degree > NB is resolved by the
+// whole warp (nbr_components_warp).
+template <int H, u32 U>
+__device__ __forceinline__ void score_bm(const Sim<false> &g, const Cmd &cmd, u32 wrank, u32 wsize, Cand &best,
+                                         u32 &bk, u64 &bytes, u64 &evals, u32 *slown) {
+  const u32 FULL = 0xffffffffu, lane = threadIdx.x & 31;
+  const u32 nwords = (cmd.n_ids + 31) / 32;
+  constexpr bool NBR = H == H_DTR || H == H_DTR_EQ || H == H_ABL;
+  for (u32 w0 = wrank; w0 < nwords; w0 += U * wsize) {
+    u32 bits[U];
+    uint4 sr[U];
+#pragma unroll
+    for (u32 j = 0; j < U; j++) {          // bitmap words and score records, all in flight
+      const u32 w = w0 + j * wsize, t = w * 32 + lane;
+      bits[j] = w < nwords ? g.pool_word(w) : 0u;
+      sr[j] = t < cmd.n_ids ? g.srec(t) : make_uint4(0, 0, 0, 0);
     }
-    Cand c[K];
-    if constexpr (!SM && BM && (H == H_DTR || H == H_DTR_EQ)) {
 #pragma unroll
-      for (u32 r = 0; r < K; r += 2)
-        if (r < k) score_pair_dtr<H == H_DTR_EQ>(g, cmd, cand + r, k - r < 2 ? k - r : 2, c + r, bytes);
-    } else {
-#pragma unroll
-      for (u32 r = 0; r < K; r++)
-        if (r < k) score_h<SM, H>(g, cmd, cand[r], c[r], bytes);
+    for (u32 j = 0; j < U; j++) {
+      const bool in = (bits[j] >> lane) & 1u;
+      Cand c;
+      c.id = (w0 + j * wsize) * 32 + lane;
+      if constexpr (NBR) {
+        const bool slow = in && sr[j].w != 0;    // evicted neighbours: phase 2
+        const u32 m = __ballot_sync(FULL, slow);
+        if (m) {
+          u32 at = 0;
+          if (lane == 0) at = atomicAdd(slown, (u32)__popc(m));
+          at = __shfl_sync(FULL, at, 0);
+          if (slow) g.m.w(g.L.slowq + at + __popc(m & ((1u << lane) - 1))) = c.id;
+        }
+        if (!in || slow) continue;
+        evals++;
+        bytes += 16;
+        if constexpr (H == H_ABL) {
+          abl_finish(abl_c(cmd.heur) == ABL_NO ? 1ull : (u64)sr[j].y, sr[j].x, sr[j].z, cmd, c);
+        } else {
+          stale_score((u64)sr[j].y, sr[j].x, sr[j].z, cmd.clock, c.num, c.den);
+        }
+      } else {
+        if (!in) continue;
+        evals++;
+        if constexpr (H == H_LRU) {
+          stale_score(1, 1, sr[j].z, cmd.clock, c.num, c.den);
+          bytes += 4;
+        } else if constexpr (H == H_SIZE) {
+          c.num = 1; c.den = sr[j].x;
+          bytes += 4;
+        } else if constexpr (H == H_LOCAL) {
+          stale_score((u64)sr[j].y, sr[j].x, sr[j].z, cmd.clock, c.num, c.den);
+          bytes += 12;
+        } else {
+          c.num = splitmix64(cmd.seed ^ (cmd.decisions << 32) ^ (u64)c.id); c.den = 1;
+          bytes += 4;
+        }
+      }
+      cand_take(best, bk, c, int_key_heur(H));
     }
-#pragma unroll
-    for (u32 r = 0; r < K; r++)
-      if (r < k) cand_take(best, bk, c[r]);
-    evals += k;
+  }
+  if constexpr (NBR) {
+    cg::this_grid().sync();
+    // phase 2: warp w takes queue entries [32 w, 32 w + 32), [32 (w + W), ...):
+    // one candidate per lane (phased gathers); degree > NB: the whole warp
+    const u32 ns = __ldcg(slown);
+    constexpr bool UF = H != H_DTR;
+    for (u32 i0 = wrank * 32; i0 < ns; i0 += wsize * 32) {
+      const u32 i = i0 + lane;
+      const u32 t = i < ns ? __ldcg(&g.m.w(g.L.slowq + i)) : NONE;
+      uint4 sr = make_uint4(0, 0, 0, 0), ar = make_uint4(0, 0, 0, 0);
+      if (t != NONE) { sr = g.srec(t); ar = g.arec(t); }
+      const bool big = t != NONE && ar.y + ar.w > NB;
+      auto finish = [&](u32 tt, const uint4 &s4, u64 sum, u32 L) {
+        Cand c;
+        c.id = tt;
+        evals++;
+        bytes += 16;
+        if constexpr (H == H_ABL) abl_finish((u64)s4.y + sum, s4.x, s4.z, cmd, c);
+        else stale_score((u64)s4.y + sum, s4.x, L, cmd.clock, c.num, c.den);
+        cand_take(best, bk, c);
+      };
+      if (t != NONE && !big) {
+        u64 sum;
+        u32 L;
+        nbr_components_phased<UF>(g, sr, ar, sum, L, bytes);
+        finish(t, sr, sum, L);
+      }
+      u32 bm = __ballot_sync(FULL, big);
+      while (bm) {
+        const u32 l = __ffs(bm) - 1;
+        bm &= bm - 1;
+        const u32 tt = __shfl_sync(FULL, t, l);
+        uint4 s4;
+        s4.x = __shfl_sync(FULL, sr.x, l); s4.y = __shfl_sync(FULL, sr.y, l);
+        s4.z = __shfl_sync(FULL, sr.z, l); s4.w = __shfl_sync(FULL, sr.w, l);
+        u64 sum;
+        u32 L;
+        nbr_components_warp<UF>(g, tt, s4, sum, L, bytes);
+        if (lane == l) finish(tt, s4, sum, L);
+      }
+    }
   }
 }
 
@@ -360,24 +512,41 @@ __device__ __forceinline__ void score_loop(const Sim<SM> &g, const Cmd &cmd, u32
 // WIDE: global-memory team (four candidates in flight per thread, else two).
 template <bool SM, bool BM, bool WIDE = false>
 __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, u32 wrank, u32 wsize,
-                           volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk) {
+                           volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk, u32 *slown = nullptr) {
   Cand best = cand_none();
   bk = KEY_NONE;
   if (BM && rank == 0) bytes += (cmd.n_ids + 7) / 8;     // the pool bitmap
   constexpr u32 K = WIDE ? 4 : 2;
+  if constexpr (!SM && BM) {
+    switch (cmd.heur) {
+      case H_DTR: score_bm<H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_DTR_EQ: score_bm<H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_LRU: score_bm<H_LRU, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_SIZE: score_bm<H_SIZE, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_LOCAL: score_bm<H_LOCAL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_RANDOM: score_bm<H_RANDOM, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      default:
+        if (is_abl(cmd.heur) && abl_c(cmd.heur) != ABL_ESTAR) {
+          score_bm<H_ABL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown);
+          return best;
+        }
+        break;
+    }
+  } else {
   switch (cmd.heur) {
-    case H_DTR: score_loop<SM, BM, H_DTR, 2>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_DTR_EQ: score_loop<SM, BM, H_DTR_EQ, 2>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_LRU: score_loop<SM, BM, H_LRU, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_SIZE: score_loop<SM, BM, H_SIZE, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_LOCAL: score_loop<SM, BM, H_LOCAL, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_RANDOM: score_loop<SM, BM, H_RANDOM, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_DTR: score_loop<SM, H_DTR, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_DTR_EQ: score_loop<SM, H_DTR_EQ, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_LRU: score_loop<SM, H_LRU, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_SIZE: score_loop<SM, H_SIZE, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_LOCAL: score_loop<SM, H_LOCAL, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_RANDOM: score_loop<SM, H_RANDOM, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
     default:
       if (is_abl(cmd.heur) && abl_c(cmd.heur) != ABL_ESTAR) {
-        score_loop<SM, BM, H_ABL, 2>(g, cmd, rank, size, best, bk, bytes, evals);
+        score_loop<SM, H_ABL, 2>(g, cmd, rank, size, best, bk, bytes, evals);
         return best;
       }
       break;
+  }
   }
   // H_MSPS: one warp per candidate
   const u32 nw = wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
@@ -394,16 +563,16 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
       const u32 t = BM ? w * 32 + b : g.pool_ids(w);
       const uint4 sr = g.srec(t);
       const bool down = cmd.heur != H_MSPS;
-      const u64 sum = msps_closure(g, sr, wrank, msps_tail + (threadIdx.x >> 5), bytes, t, down);
+      // nev = 0: no evicted neighbour, so the closure is empty
+      const u64 sum = sr.w ? msps_closure(g, g.arec(t), wrank, msps_tail + (threadIdx.x >> 5), bytes, t, down) : 0;
+      if (sr.w && lane == 0) bytes += 16;    // adjacency record
       if (lane == 0) {
         Cand c;
         c.id = t;
         if (cmd.heur == H_DTR_FULL) {            // (c(S) + sum_{e*(S)} c) / (size(S) * stale(S))
-          stale_score((u64)sr.y + sum, sr.x, g.la(t), cmd.clock, c.num, c.den);
-          bytes += 4;
+          stale_score((u64)sr.y + sum, sr.x, sr.z, cmd.clock, c.num, c.den);
         } else if (is_abl(cmd.heur)) {           // h'(s, m, e*)
-          abl_finish((u64)sr.y + sum, sr.x, g.la(t), cmd, c);
-          bytes += 4;
+          abl_finish((u64)sr.y + sum, sr.x, sr.z, cmd, c);
         } else {                                 // MSPS and h_e* (P:1835-1837): (c0 + sum) / m
           c.num = (u64)sr.y + sum;
           c.den = sr.x;
@@ -430,13 +599,13 @@ __device__ void team_scores_out(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 
     for (u32 i = wr; i < P; i += nw) {
       const u32 t = g.pool_ids(i);
       const uint4 sr = g.srec(t);
-      const u64 sum = msps_closure(g, sr, wr, msps_tail + (threadIdx.x >> 5), junk, t, cmd.heur != H_MSPS);
+      const u64 sum = sr.w ? msps_closure(g, g.arec(t), wr, msps_tail + (threadIdx.x >> 5), junk, t, cmd.heur != H_MSPS) : 0;
       if (lane == 0) {
         u64 num = (u64)sr.y + sum, den = sr.x;
-        if (cmd.heur == H_DTR_FULL) stale_score((u64)sr.y + sum, sr.x, g.la(t), cmd.clock, num, den);
+        if (cmd.heur == H_DTR_FULL) stale_score((u64)sr.y + sum, sr.x, sr.z, cmd.clock, num, den);
         if (is_abl(cmd.heur)) {
           Cand c;
-          abl_finish((u64)sr.y + sum, sr.x, g.la(t), cmd, c);
+          abl_finish((u64)sr.y + sum, sr.x, sr.z, cmd, c);
           num = c.num; den = c.den;
         }
         onum[i] = num; oden[i] = den; oid[i] = t;
@@ -480,14 +649,14 @@ struct RedSmem {
 };
 
 // block-wide argmin; the result is valid in warp 0 (all lanes) after return.
-__device__ __forceinline__ Cand block_argmin(const Cand &c, u32 k, RedSmem &sm) {
-  Cand w = warp_argmin_fast(c, k);
+__device__ __forceinline__ Cand block_argmin(const Cand &c, u32 k, RedSmem &sm, bool ik = false) {
+  Cand w = warp_argmin_fast(c, k, ik);
   const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   if (lane == 0) sm.warp[wid] = w;
   __syncthreads();
   if (wid == 0) {
     w = lane < nw ? sm.warp[lane] : cand_none();
-    w = warp_argmin_fast(w, cand_key(w));
+    w = warp_argmin_fast(w, cand_key(w, ik), ik);
   }
   return w;
 }
