@@ -269,6 +269,13 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
         PROF_ADD(0, t1 - t0);
       }
       c = shfl_cmd(c);
+      if (c.kind == CMD_ARGMIN && c.pool_size <= WARP_TEAM_MAX && g.L.pool_key) {   // size / LRU: 64-bit keys
+        PROF_T(t2);
+        const u64 k = warp_min64(team_intkey_min(g, c, lane, 32, bytes, evals));
+        PROF_T(t3);
+        if (lane == 0) { res = intkey_cand(g, c, k); have = true; PROF_ADD(1, t3 - t2); PROF_ADD(3, 1); }
+        continue;
+      }
       if (c.kind == CMD_ARGMIN && c.pool_size <= WARP_TEAM_MAX) {
         PROF_T(t2);
         u32 bk;

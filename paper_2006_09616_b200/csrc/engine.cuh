@@ -26,7 +26,8 @@
 //              order, so a warp's candidates are consecutive ids whose (mostly
 //              nearby) neighbours share sectors and L1 lines
 //   state: bit31 material (t.m = T), bit30 computed once (reading C-19),
-//          bit29 V1-banished, bits 0..28 label of t's evicted component (h_DTR)
+//          bit29 V1-banished, bits 0..28 label of t's evicted component (h_DTR;
+//          a label is a slot of the component table, recycled through a free stack)
 //   la:    last_access + 1, 0 = -inf (banish_V2)
 //   nev:   number of t's neighbours (parents, children) that are evicted --
 //          maintained by the leader on evict / rematerialize / V1 banish for the
@@ -63,6 +64,10 @@ __host__ __device__ __forceinline__ bool valid_heuristic(u32 h) { return h <= H_
 __host__ __device__ __forceinline__ bool uses_closure(u32 h) {
   return h == H_MSPS || h == H_DTR_FULL || h == H_ESTAR || (is_abl(h) && abl_c(h) == ABL_ESTAR);
 }
+// Integer keys (ik): h_size and h_LRU scores are 1/m and 1/s with integer m, s,
+// so they order exactly by an integer: ~m, resp. la (encoded last access; 0 =
+// -inf gives score 0, clock + 1 gives s = 0 = +inf); no division is needed.
+__host__ __device__ __forceinline__ bool int_key_heur(u32 h) { return h == H_SIZE || h == H_LRU; }
 // union-find evicted components
 __host__ __device__ __forceinline__ bool uses_uf(u32 h) { return h == H_DTR_EQ || (is_abl(h) && abl_c(h) == ABL_EQCLASS); }
 enum { OP_MAKE = 1, OP_GET = 2, OP_RELEASE = 3, OP_REMAT = 4, OP_ENSURE = 5, OP_DEBUG_EVICT = 6,
@@ -81,7 +86,9 @@ __host__ __device__ __forceinline__ bool is_material(u32 s) { return (s & M_BIT)
 struct Lay {
   u32 n, E, heur, linked, track_nev;
   u32 srec, arec, par, ch, state, rho, ell, pool_bm, pool_words, pool_ids, pool_pos, fr, pb;
+  u32 pool_key;                                        // compact list, size/LRU: u64 key per slot (0 = none)
   u32 mem_next, comp, comp_head, bfs_q, stamp;         // h_DTR (comp rec: {cost lo, cost hi, maxla, size})
+  u32 mem_prev, comp_free;                             // h_DTR: member lists are doubly linked; free label slots
   u32 node_of, uf, uf_size, uf_cap;                    // h_DTR_eq (uf rec: {cost lo, cost hi, maxla, parent})
   u32 msps_bm, msps_q, msps_words, msps_warps;         // h_MSPS per-warp scratch
   u32 e_next, e_child;                                 // linked children (per-call)
@@ -109,14 +116,18 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
   L.pool_bm = take(L.pool_words);
   L.pool_ids = take(n1);
   L.pool_pos = take(n1);
+  L.pool_key = (int_key_heur(heur) && !grid) ? take(2 * n1) : 0;
   L.fr = take(4 * n1);
   L.pb = take(e1);
   L.mem_next = L.comp = L.comp_head = L.bfs_q = L.stamp = 0;
+  L.mem_prev = L.comp_free = 0;
   L.node_of = L.uf = L.uf_size = L.uf_cap = 0;
   L.msps_bm = L.msps_q = L.msps_words = L.msps_warps = 0;
   L.e_next = L.e_child = 0;
   if (heur == H_DTR) {
     L.mem_next = take(n1);
+    L.mem_prev = take(n1);
+    L.comp_free = take(n1);
     L.comp = take(4 * n1);
     L.comp_head = take(n1);
     L.bfs_q = take(n1);
@@ -185,7 +196,8 @@ struct Scalars {
   u32 pending_op;     // per-call: the op word being applied
   u32 n_scores;       // per-call OP_SCORES: pool size scored
   u32 dealloc;        // DEALLOC_*: what release does at rho = 0 (reading C-22)
-  u32 pad[2];
+  u32 comp_top;       // h_DTR: free label slots on the stack
+  u32 comp_fresh;     // h_DTR: label slots never used yet
   u64 kill_limit;     // thrash_kill * base_so_far (recomputed at every MAKE); 0 = off
 };
 

@@ -43,6 +43,11 @@ struct Leader {
 
   // ------------------------------------------------------------- pool
   // R.pool: bitmap over tensor ids (BM) or compact list with positions
+  // size / LRU over a compact list: the slot's exact integer key (engine.cuh)
+  __device__ __forceinline__ uint2 pool_key_of(u32 t) {
+    const uint4 sr = g.srec(t);
+    return make_uint2(t, s.heuristic == H_SIZE ? ~sr.x : sr.z);
+  }
   __device__ __forceinline__ void pool_add(u32 t) {
     if constexpr (BM) {
       g.pool_word(t >> 5) |= 1u << (t & 31);
@@ -51,6 +56,16 @@ struct Leader {
       const u32 k = s.pool_size++;
       g.pool_pos(t) = k;
       g.pool_ids(k) = t;
+      if (g.L.pool_key) g.m.d(g.L.pool_key + 2 * k) = pool_key_of(t);
+    }
+  }
+  // la(t) changed: refresh t's key if it is a pool member (LRU)
+  __device__ __forceinline__ void pool_rekey(u32 t) {
+    if constexpr (!BM) {
+      if (g.L.pool_key && s.heuristic == H_LRU) {
+        const u32 p = g.pool_pos(t);
+        if (p != NONE) g.m.d(g.L.pool_key + 2 * p) = pool_key_of(t);
+      }
     }
   }
   __device__ __forceinline__ void pool_remove(u32 t) {
@@ -66,6 +81,7 @@ struct Leader {
       g.pool_ids(p) = last;
       g.pool_pos(last) = p;
       g.pool_pos(t) = NONE;
+      if (g.L.pool_key) g.m.d(g.L.pool_key + 2 * p) = g.m.d(g.L.pool_key + 2 * s.pool_size);
     }
   }
   __device__ __forceinline__ bool pool_has(u32 t) {
@@ -151,27 +167,41 @@ struct Leader {
   }
 
   // ------------------------------------------------------------- exact components
-  // merge component b into a (a, b labels; a is kept when a is not smaller)
+  // Component labels are slots of the component table, taken from a free stack
+  // (or the never-used range) and returned when a component is absorbed or
+  // dissolved; member lists are doubly linked.
+  __device__ __forceinline__ u32 comp_alloc() {
+    if (s.comp_top) return g.m.w(g.L.comp_free + --s.comp_top);
+    return s.comp_fresh++;
+  }
+  __device__ __forceinline__ void comp_release(u32 c) { g.m.w(g.L.comp_free + s.comp_top++) = c; }
+
+  // merge component b into a (a, b labels; the larger keeps its label)
   __device__ __forceinline__ u32 comp_merge(u32 a, u32 b) {
     uint4 ca = g.comp(a), cb = g.comp(b);
     if (ca.w < cb.w) { u32 x = a; a = b; b = x; uint4 y = ca; ca = cb; cb = y; }
     u32 x = g.m.w(g.L.comp_head + b), last = NONE;
     while (x != NONE) { g.state(x) = O_BIT | a; last = x; x = g.m.w(g.L.mem_next + x); }
-    g.m.w(g.L.mem_next + last) = g.m.w(g.L.comp_head + a);
+    const u32 ha = g.m.w(g.L.comp_head + a);
+    g.m.w(g.L.mem_next + last) = ha;
+    if (ha != NONE) g.m.w(g.L.mem_prev + ha) = last;
     g.m.w(g.L.comp_head + a) = g.m.w(g.L.comp_head + b);
     u64 cost = mk64(ca.x, ca.y) + mk64(cb.x, cb.y);
     g.comp(a) = make_uint4((u32)cost, (u32)(cost >> 32), ca.z > cb.z ? ca.z : cb.z, ca.w + cb.w);
+    comp_release(b);
     return a;
   }
 
   // t has just become evicted: {t} joins the components of its evicted neighbours.
   // (fused: every neighbour's nev += 1)
   __device__ __forceinline__ void evict_exact(u32 t, const uint4 &sr, const uint4 &ar) {
-    g.comp(t) = make_uint4(sr.y, 0, sr.z, 1);
-    g.m.w(g.L.comp_head + t) = t;
+    const u32 c0 = comp_alloc();
+    g.comp(c0) = make_uint4(sr.y, 0, sr.z, 1);
+    g.m.w(g.L.comp_head + c0) = t;
     g.m.w(g.L.mem_next + t) = NONE;
-    g.state(t) = O_BIT | t;
-    u32 cur = t;
+    g.m.w(g.L.mem_prev + t) = NONE;
+    g.state(t) = O_BIT | c0;
+    u32 cur = c0;
     g.for_each_nbr(t, ar, [&](u32 q) {
       g.nev(q) += 1;
       u32 sq = g.state(q);
@@ -181,15 +211,41 @@ struct Leader {
     });
   }
 
-  // t (formerly in component c) has just become material: relabel c \ {t} by
-  // BFS from t's evicted neighbours; each BFS tree becomes a component labelled
-  // by its root (a member).
+  // max last_access over the members of c (la encoded, 0 = -inf)
+  __device__ __forceinline__ u32 comp_rescan_maxla(u32 c) {
+    u32 mx = 0;
+    for (u32 x = g.m.w(g.L.comp_head + c); x != NONE; x = g.m.w(g.L.mem_next + x)) {
+      const u32 l = g.la(x);
+      mx = l > mx ? l : mx;
+    }
+    return mx;
+  }
+
+  // t (formerly in component c, with k = nev(t) evicted neighbours) has just
+  // stopped being evicted.  k = 0: c was {t}.  k = 1: t was a leaf of c, which
+  // stays connected -- unlink t, subtract its cost, rescan the max la only if
+  // t held it.  k >= 2: relabel c \ {t} by BFS from t's evicted neighbours;
+  // each BFS tree becomes a component with a fresh label.
   __device__ __forceinline__ void remat_exact(u32 t, const uint4 &ar, u32 c) {
-    if (g.comp(c).w == 1) return;
+    const uint4 cc = g.comp(c);
+    if (cc.w == 1) { comp_release(c); return; }
+    if (g.nev(t) == 1) {
+      const u32 p = g.m.w(g.L.mem_prev + t), nx = g.m.w(g.L.mem_next + t);
+      if (p != NONE) g.m.w(g.L.mem_next + p) = nx;
+      else g.m.w(g.L.comp_head + c) = nx;
+      if (nx != NONE) g.m.w(g.L.mem_prev + nx) = p;
+      const uint4 st = g.srec(t);
+      const u64 cost = mk64(cc.x, cc.y) - st.y;
+      const u32 mx = st.z == cc.z ? comp_rescan_maxla(c) : cc.z;
+      g.comp(c) = make_uint4((u32)cost, (u32)(cost >> 32), mx, cc.w - 1);
+      return;
+    }
+    comp_release(c);
     u32 ep = ++s.epoch;
     g.for_each_nbr(t, ar, [&](u32 q) {
       u32 sq = g.state(q);
       if (!is_evicted(sq) || g.m.w(g.L.stamp + q) == ep) return;
+      const u32 nc = comp_alloc();
       u32 head = 0, tail = 0;
       g.m.w(g.L.bfs_q + tail++) = q;
       g.m.w(g.L.stamp + q) = ep;
@@ -199,8 +255,10 @@ struct Leader {
         u32 x = g.m.w(g.L.bfs_q + head++);
         const uint4 sx = g.srec(x);
         const uint4 ax = g.arec(x);
-        g.state(x) = O_BIT | q;
+        g.state(x) = O_BIT | nc;
         g.m.w(g.L.mem_next + x) = list;
+        g.m.w(g.L.mem_prev + x) = NONE;
+        if (list != NONE) g.m.w(g.L.mem_prev + list) = x;
         list = x;
         size++;
         cost += sx.y;
@@ -212,22 +270,16 @@ struct Leader {
           }
         });
       }
-      g.m.w(g.L.comp_head + q) = list;
-      g.comp(q) = make_uint4((u32)cost, (u32)(cost >> 32), mx, size);
+      g.m.w(g.L.comp_head + nc) = list;
+      g.comp(nc) = make_uint4((u32)cost, (u32)(cost >> 32), mx, size);
     });
   }
 
   // V2 release of an evicted tensor: its la dropped to -inf; rescan the max if it was the max.
   __device__ __forceinline__ void lower_maxla_exact(u32 t, u32 old) {
     u32 c = g.state(t) & COMP_MASK;
-    uint4 cr = g.comp(c);
-    if (old != cr.z) return;
-    u32 mx = 0;
-    for (u32 x = g.m.w(g.L.comp_head + c); x != NONE; x = g.m.w(g.L.mem_next + x)) {
-      u32 l = g.la(x);
-      mx = l > mx ? l : mx;
-    }
-    g.comp(c).z = mx;
+    if (old != g.comp(c).z) return;
+    g.comp(c).z = comp_rescan_maxla(c);
   }
 
   // ------------------------------------------------------------- union-find
@@ -481,6 +533,7 @@ struct Leader {
         for (u32 j = 0; j < pr.y; j++) {          // p.C u= {t}; p.last_accessed := clock
           u32 p = g.par(pr.x + j);
           g.la(p) = now;
+          pool_rekey(p);
           u32 sp = g.state(p);
           if (is_evicted(sp)) raise_maxla(p, sp, now);
         }
@@ -504,6 +557,7 @@ struct Leader {
           if (s.dealloc == DEALLOC_V2) {              // banish_V2
             u32 old = g.la(id);
             g.la(id) = 0;
+            pool_rekey(id);
             if (s.heuristic == H_DTR && is_evicted(g.state(id))) lower_maxla_exact(id, old);
           } else if (s.dealloc == DEALLOC_V1) {
             maybe_banish(id);

@@ -149,7 +149,6 @@ constexpr u32 KEY_NONE = 0xFFFFFFFFu, KEY_INF = 0x7F800000u, KEY_MARGIN = 256u; 
 // Integer keys (ik): h_size and h_LRU scores are 1/m and 1/s with integer m, s,
 // so key = ~den orders them exactly (score 0 -> 0, +inf -> 0xFFFFFFFE); equal
 // keys are still resolved exactly, so the margin is 0 and no division is done.
-__host__ __device__ __forceinline__ bool int_key_heur(u32 h) { return h == H_SIZE || h == H_LRU; }
 
 __device__ __forceinline__ u32 cand_key(const Cand &c, bool ik = false) {
   if (c.id == NONE) return KEY_NONE;
@@ -507,6 +506,41 @@ __device__ __forceinline__ void score_bm(const Sim<false> &g, const Cmd &cmd, u3
   }
 }
 
+// h_size / h_LRU over the compact list: every pool slot carries its exact
+// 64-bit key (integer score key << 32 | id, leader.cuh pool_key_of), so the
+// scan is a plain 64-bit min and the winner's (num, den) is rebuilt from its
+// record.  ~0 = no candidate.
+template <bool SM>
+__device__ __forceinline__ u64 team_intkey_min(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, u64 &bytes,
+                                               u64 &evals) {
+  u64 kmin = ~0ull;
+  u32 cnt = 0;
+#pragma unroll 4
+  for (u32 i = rank; i < cmd.pool_size; i += size) {
+    const uint2 k = g.m.d(g.L.pool_key + 2 * i);
+    const u64 kk = mk64(k.x, k.y);
+    kmin = kk < kmin ? kk : kmin;
+    cnt++;
+  }
+  bytes += 8ull * cnt;
+  evals += cnt;
+  return kmin;
+}
+__device__ __forceinline__ u64 warp_min64(u64 k) {
+  const u32 hi = (u32)(k >> 32), lo = (u32)k;
+  const u32 mh = __reduce_min_sync(0xffffffffu, hi);
+  const u32 ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xFFFFFFFFu);
+  return mk64(ml, mh);
+}
+template <bool SM>
+__device__ __forceinline__ Cand intkey_cand(const Sim<SM> &g, const Cmd &cmd, u64 k) {
+  Cand c;
+  c.id = (u32)k;
+  if (cmd.heur == H_SIZE) { c.num = 1; c.den = g.srec(c.id).x; }
+  else stale_score(1, 1, g.la(c.id), cmd.clock, c.num, c.den);
+  return c;
+}
+
 // Score every pool member of this thread's slice; return the slice argmin and
 // its key.  rank/size: thread index in the team; wrank/wsize: warp index (MSPS).
 // WIDE: global-memory team (four candidates in flight per thread, else two).
@@ -533,6 +567,11 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
         break;
     }
   } else {
+  if (g.L.pool_key) {
+    const u64 kmin = team_intkey_min(g, cmd, rank, size, bytes, evals);
+    if (kmin != ~0ull) { best = intkey_cand(g, cmd, kmin); bk = cand_key(best, true); }
+    return best;
+  }
   switch (cmd.heur) {
     case H_DTR: score_loop<SM, H_DTR, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
     case H_DTR_EQ: score_loop<SM, H_DTR_EQ, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
