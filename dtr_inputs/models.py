@@ -21,7 +21,7 @@ import math
 
 import numpy as np
 
-from .logfmt import LogBuilder, assemble, OP_MAKE, OP_SHIFT, MAX_BASE
+from .logfmt import LogBuilder, LogView, assemble, OP_MAKE, OP_SHIFT, MAX_BASE
 
 MODEL_IDS = {
     "linear": 1, "resnet32": 2, "densenet100": 3, "unet": 4, "lstm": 5,
@@ -479,6 +479,30 @@ def random_dag(n: int, seed: int = 0, window: int = 64, p_local: float = 0.9,
     cost = rng.integers(1, cost_max + 1, size=n)
     ops = (np.uint64(OP_MAKE) << np.uint64(OP_SHIFT)) | np.arange(n, dtype=np.uint64)
     return assemble(mem, cost, par_off, par, ops.astype(np.uint32),
+                    model_id=MODEL_IDS["random_dag"], seed=seed)
+
+
+def hub_dag(n: int, seed: int = 0, n_hubs: int = 16, fan: int = 80, window: int = 64) -> np.ndarray:
+    """random_dag plus hub tensors: ids 64..64+n_hubs-1 each become a parent of
+    ~fan later tensors, so hubs have degree > 32 (the whole-GPU team's
+    warp-cooperative neighbour walk).  MAKE only, like random_dag."""
+    rng = np.random.default_rng(seed)
+    base = random_dag(n, seed=seed, window=window)
+    v = LogView(base)
+    pars = [list(v.parents(t)) for t in range(n)]
+    hubs = np.arange(64, 64 + n_hubs)
+    p = n_hubs * fan / max(n - 64 - n_hubs, 1)
+    for c in range(64 + n_hubs, n):
+        if rng.random() < p:
+            h = int(hubs[rng.integers(0, n_hubs)])
+            if h not in pars[c]:
+                pars[c].append(h)
+    k = np.array([len(x) for x in pars])
+    par_off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(k, out=par_off[1:])
+    par = np.array([q for x in pars for q in x], dtype=np.int64)
+    ops = (np.uint64(OP_MAKE) << np.uint64(OP_SHIFT)) | np.arange(n, dtype=np.uint64)
+    return assemble(v.mem.astype(np.int64), v.cost.astype(np.int64), par_off, par, ops.astype(np.uint32),
                     model_id=MODEL_IDS["random_dag"], seed=seed)
 
 

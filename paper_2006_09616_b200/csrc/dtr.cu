@@ -230,17 +230,6 @@ __device__ __forceinline__ Cmd shfl_cmd(const Cmd &c) {
   return r;
 }
 
-#ifdef DTR_PROFILE
-// [0] leader resume cycles, [1] warp-team score cycles, [2] warp reduce cycles,
-// [3] warp-team decisions, [4] cta-team cycles, [5] cta-team decisions, [6] init cycles
-__device__ unsigned long long g_prof[8];
-#define PROF_T(x) unsigned long long x = clock64()
-#define PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
-#else
-#define PROF_T(x)
-#define PROF_ADD(i, v)
-#endif
-
 template <bool SM>
 __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_result *row, dtr_evict_rec *trace,
                         CtaShared &sh) {
@@ -831,8 +820,8 @@ int dtr_version(void) { return 1; }
 
 #ifdef DTR_PROFILE
 int dtr_debug_profile(unsigned long long *out, int reset) {
-  CK(cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 8));
-  if (reset) { unsigned long long z[8] = {0}; CK(cudaMemcpyToSymbol(g_prof, z, sizeof z)); }
+  CK(cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 16));
+  if (reset) { unsigned long long z[16] = {0}; CK(cudaMemcpyToSymbol(g_prof, z, sizeof z)); }
   return DTR_OK;
 }
 #endif

@@ -38,6 +38,19 @@
 #pragma once
 #include <stdint.h>
 
+#ifdef DTR_PROFILE
+// clock64 phase counters (probe builds only, scripts/probe_prof*.py):
+// [0] leader resume cycles, [1] warp-team score cycles, [2] warp reduce cycles,
+// [3] warp-team decisions, [4] cta-team cycles, [5] cta-team decisions, [6] init cycles,
+// [8/9] record_and_evict cycles/calls, [10/11] complete_top, [12/13] push, [14] resume loop iterations
+__device__ unsigned long long g_prof[16];
+#define PROF_T(x) unsigned long long x = clock64()
+#define PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
+#else
+#define PROF_T(x)
+#define PROF_ADD(i, v)
+#endif
+
 namespace dtr {
 
 typedef uint32_t u32;

@@ -482,18 +482,27 @@ struct Leader {
 
   // ------------------------------------------------------------- the state machine
   __device__ __forceinline__ u32 resume(bool have, const Cand &res) {
-    if (phase == PH_FREE && have) record_and_evict(res);
+    if (phase == PH_FREE && have) {
+      PROF_T(p0);
+      record_and_evict(res);
+      PROF_T(p1);
+      PROF_ADD(8, p1 - p0); PROF_ADD(9, 1);
+    }
     if (phase == PH_SCORED) { finish_op(); phase = PH_OP; }
     for (;;) {
       if (phase == PH_GI || phase == PH_FREE) {
+        PROF_ADD(14, 1);
         if (s.sp == 0) { finish_op(); phase = PH_OP; continue; }
         const u32 k = s.sp - 1;
         uint4 fr = g.m.q(g.L.fr + 4 * k);
         if (phase == PH_GI && fr.w < fr.z) {
           g.m.w(g.L.fr + 4 * k + 3) = fr.w + 1;
           u32 p = g.m.w(g.L.pb + fr.y + fr.w);
+          PROF_T(u0);
           if (is_material(g.state(p))) lock(p);
           else push(p, g.prec(p));
+          PROF_T(u1);
+          PROF_ADD(12, u1 - u0); PROF_ADD(13, 1);
           continue;
         }
         u32 t = fr.x;
@@ -505,7 +514,10 @@ struct Leader {
           return CMD_ARGMIN;
         }
         phase = PH_GI;
+        PROF_T(c0);
         if (!complete_top(t, fr)) return CMD_DONE;
+        PROF_T(c1);
+        PROF_ADD(10, c1 - c0); PROF_ADD(11, 1);
         continue;
       }
       if (phase == PH_DONE) return CMD_DONE;

@@ -178,7 +178,6 @@ __device__ __forceinline__ Cand shfl_cand(const Cand &c, int src) {
   return r;
 }
 
-__device__ __forceinline__ Cand warp_argmin(Cand c);   // exact (below)
 
 // warp-wide exact argmin using the key fast path; every lane gets the result.
 __device__ __forceinline__ Cand warp_argmin_fast(const Cand &c, u32 k, bool ik = false) {
@@ -199,8 +198,14 @@ __device__ __forceinline__ Cand warp_argmin_fast(const Cand &c, u32 k, bool ik =
   const u32 idref = __reduce_min_sync(FULL, in ? c.id : NONE);
   const Cand ref = shfl_cand(c, __ffs(__ballot_sync(FULL, in && c.id == idref)) - 1);
   const bool below = in && score_less(c, ref);
-  if (__ballot_sync(FULL, below) == 0) return ref;
-  return warp_argmin(below ? c : cand_none());
+  u32 bm = __ballot_sync(FULL, below);
+  Cand b = ref;
+  while (bm) {                                     // the strictly-smaller contenders, exactly
+    const Cand x = shfl_cand(c, __ffs(bm) - 1);
+    bm &= bm - 1;
+    if (cand_less(x, b)) b = x;
+  }
+  return b;
 }
 
 // h'(s, m, c) = c / (m * s) with ablated measures = 1 (reading C-23)
@@ -355,7 +360,10 @@ __device__ __forceinline__ void nbr_components_warp(const Sim<false> &g, u32 t, 
     for (u32 b0 = 0; b0 < base; b0 += 32) {         // earlier chunks (degree > 32)
       u64 junk = 0;
       const u32 prev = label(b0 + lane, junk);
-      for (u32 k = 0; k < 32; k++) first = first && __shfl_sync(FULL, prev, k) != lab;
+      for (u32 k = 0; k < 32; k++) {             // every lane shuffles (no short-circuit around a sync op)
+        const u32 x = __shfl_sync(FULL, prev, k);
+        first = first && x != lab;
+      }
     }
     if (first) {
       const uint4 r = UF ? g.uf(lab) : g.comp(lab);
@@ -671,18 +679,6 @@ __device__ void team_scores_out(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 
 // ---------------------------------------------------------------------------
 // Reductions
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ Cand warp_argmin(Cand c) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    Cand d;
-    d.num = __shfl_xor_sync(0xffffffffu, c.num, o);
-    d.den = __shfl_xor_sync(0xffffffffu, c.den, o);
-    d.id = __shfl_xor_sync(0xffffffffu, c.id, o);
-    if (cand_less(d, c)) c = d;
-  }
-  return c;
-}
-
 struct RedSmem {
   Cand warp[32];
 };

@@ -13,7 +13,7 @@ for s in specs:
         continue
     b = P.DeviceBatch(logs, [s], engine=P.ENGINE_CTA)
     b.run(); torch.cuda.synchronize()
-    buf = np.zeros(8, np.uint64)
+    buf = np.zeros(16, np.uint64)
     P.lib.dtr_debug_profile(buf.ctypes.data, 1)
     b.run(); torch.cuda.synchronize()
     P.lib.dtr_debug_profile(buf.ctypes.data, 1)
@@ -21,4 +21,6 @@ for s in specs:
     d = int(r["decisions"])
     print(f"h={s['heuristic']} B={s['budget']} dec={d} remats={int(r['remats'])} st={int(r['status'])} "
           f"resume={buf[0]/1e6:.2f}M cyc ({buf[0]/max(d,1):.0f}/dec) wscore={buf[1]/max(buf[3],1):.0f}/dec "
-          f"wred={buf[2]/max(buf[3],1):.0f}/dec wdec={buf[3]} cta={buf[4]/max(buf[5],1):.0f}/dec ctadec={buf[5]} init={buf[6]}")
+          f"wred={buf[2]/max(buf[3],1):.0f}/dec wdec={buf[3]} cta={buf[4]/max(buf[5],1):.0f}/dec ctadec={buf[5]} init={buf[6]}\n"
+          f"    rec+evict {buf[8]/max(buf[9],1):.0f} x{buf[9]/max(d,1):.2f}/dec, complete_top {buf[10]/max(buf[11],1):.0f} x{buf[11]/max(d,1):.2f}/dec, "
+          f"lock/push {buf[12]/max(buf[13],1):.0f} x{buf[13]/max(d,1):.2f}/dec, loop iters {buf[14]/max(d,1):.2f}/dec")

@@ -481,3 +481,26 @@ def test_config4_lstm_full_size_sample(P, oracle_mod):
     B = v.peak_total * 100000 // v.n
     specs = [dict(log=0, h=h, budget=B, max_decisions=300) for h in ("dtr", "dtr_eq", "lru", "size")]
     assert_parity(P, oracle_mod, [w], specs, 2)
+
+
+def test_grid_engine_hub_degrees(P, oracle_mod):
+    """Hub tensors of degree > 32 (hub_dag): the whole-GPU team's warp-cooperative
+    neighbour walk (several 32-neighbour chunks, labels deduplicated across
+    chunks) and the per-lane phased walk, on the grid engine and dtr_pool_argmin."""
+    import torch
+    w = models.hub_dag(20000, seed=5)
+    v = LogView(w)
+    specs = [dict(log=0, h=h, budget=v.peak_total * pm // 1000, max_decisions=600)
+             for h in ("dtr", "dtr_eq", "abl_eqclass_ms") for pm in (930, 970)]
+    assert_parity(P, oracle_mod, [w], specs, 2)
+    for h in ("dtr", "dtr_eq"):
+        D = 300
+        B = v.peak_total * 950 // 1000
+        ref, tr = oracle_mod.replay(w, oracle_mod.HEURISTICS[h], B, max_decisions=D + 1, trace_cap=D + 1)
+        b = P.DeviceBatch([w], [dict(log=0, budget=B, heuristic=P.HEURISTICS[h], max_decisions=D)],
+                          engine=P.ENGINE_GRID)
+        b.run()
+        out = b.pool_argmin().cpu().numpy().astype(np.uint64)
+        torch.cuda.synchronize()
+        nxt = tr[D]
+        assert (int(out[0]), int(out[1]), int(out[2])) == (int(nxt["num"]), int(nxt["den"]), int(nxt["id"])), h
