@@ -19,6 +19,8 @@ when N > 1].
   roofline_large_pool: K3+K4 alone (dtr_pool_argmin: score pass + exact argmin)
             over the ~1e6-tensor pool of the config-5s stress log after 1000 grid-engine
             decisions; algorithmic bytes per launch / CUDA-event launch time.
+  roofline_large_pool_4e6: the same at the 4e6-tensor point whose working set
+            exceeds the 126 MB L2 (cost U[1,60] keeps base <= 2^27).
   cpu_baseline: the CPU oracle (oracle/, plain C, unmodified) on the host cores,
             process pool, bounded sample of the same cells (rank 0, N = 1 only).
 
@@ -201,6 +203,7 @@ def main():
     ap.add_argument("--no-large-pool", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--large-n", type=int, default=1000000)
+    ap.add_argument("--large-n2", type=int, default=4000000, help="second large-pool point (0 = skip)")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-4 / config-5 extra measurements")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -339,6 +342,8 @@ def main():
 
     if rank == 0 and not args.no_large_pool:
         out["roofline_large_pool"] = large_pool(P, torch, dev, args.large_n, hbm_peak, peak_src)
+        if args.large_n2:   # the point that exceeds the 126 MB L2
+            out["roofline_large_pool_4e6"] = large_pool(P, torch, dev, args.large_n2, hbm_peak, peak_src)
     if rank == 0 and ws == 1 and not args.no_extra:
         out["config4_single_run"] = config4(P, torch, dev)
         out["config5_sweep_sample"] = config5(P, torch, dev)
@@ -413,7 +418,8 @@ def large_pool(P, torch, dev, n, hbm_peak, peak_src, D=1000, reps=20):
     up to its D-th eviction decision (h_DTR), then time dtr_pool_argmin -- the
     score pass + exact argmin over the resident pool -- with CUDA events, L2
     flushed (256 MiB write) before every launch."""
-    w = models.random_dag(n, seed=0)
+    # cost U[1,200] keeps base <= 2^27 up to ~1.3e6 tensors; beyond, U[1,60] (SURVEY 8(d) 5s)
+    w = models.random_dag(n, seed=0, cost_max=200 if n <= 1300000 else 60)
     v = LogView(w)
     spec = [dict(log=0, budget=v.peak_total * 98 // 100, heuristic=0, thrash_kill=16, max_decisions=D)]
     b = P.DeviceBatch([w], spec, engine=P.ENGINE_GRID)
@@ -438,8 +444,7 @@ def large_pool(P, torch, dev, n, hbm_peak, peak_src, D=1000, reps=20):
     ach = float(o[3]) / t / 1e9
     traffic = None
     try:
-        if n == 1000000:
-            traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get("pool_argmin_1e6")
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(f"pool_argmin_{n}")
     except Exception:
         pass
     return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
