@@ -144,6 +144,7 @@ __device__ void init_scalars(Scalars &s, const dtr_cell &cell) {
   s.cell_id = cell.cell_id;
   s.dealloc = cell.dealloc;
   s.trace_hash = 14695981039346656037ull;
+  norm_scalars(s);
 }
 
 __device__ void write_row(dtr_result &r, const Scalars &s, u64 bytes, u64 evals) {
@@ -665,6 +666,7 @@ __device__ void run_adversary(const dtr_adversary &run, u32 *gbase, dtr_result *
     L.s.B = B; L.s.seed = run.seed; L.s.trace_cap = run.trace_cap; L.s.trace_off = run.trace_offset;
     L.s.heuristic = run.heuristic; L.s.cell_id = run.cell_id;
     L.s.trace_hash = 14695981039346656037ull;
+    norm_scalars(L.s);
     L.ops = nullptr;
     L.trace = (trace && run.trace_cap) ? trace + run.trace_offset : nullptr;
     L.post = 0; L.root = 0; L.percall = 1; L.free_size = 0;
@@ -1121,6 +1123,7 @@ int dtr_create(const dtr_config *cfg, dtr_runtime **out) {
   s.B = cfg->budget; s.seed = cfg->seed; s.max_decisions = cfg->max_decisions; s.trace_cap = cfg->trace_cap;
   s.heuristic = cfg->heuristic; s.thrash_kill = cfg->thrash_kill; s.dealloc = cfg->dealloc;
   s.trace_hash = 14695981039346656037ull;
+  norm_scalars(s);
   e = cudaMemcpyAsync(rt->d_sc, &s, sizeof s, cudaMemcpyHostToDevice, rt->st);
   if (e != cudaSuccess) { dtr_destroy(rt); return cuda_fail(e); }
   int rc = rt_launch(rt, 1, 0);

@@ -193,7 +193,7 @@ struct Mem {
 // ---------------------------------------------------------------------------
 struct Scalars {
   u64 clock, M, B, peak_M, base_so_far, decisions, remats, computations, trace_hash, trace_n;
-  u64 max_decisions, seed, trace_cap, trace_off;
+  u64 max_decisions, seed, trace_cap, trace_off;   // max_decisions: 0 = none (stored as ~0, norm_scalars)
   u32 n_alloc;        // tensors created (MAKE started)
   u32 pool_size;
   u32 status;         // sticky run status
@@ -211,8 +211,15 @@ struct Scalars {
   u32 dealloc;        // DEALLOC_*: what release does at rho = 0 (reading C-22)
   u32 comp_top;       // h_DTR: free label slots on the stack
   u32 comp_fresh;     // h_DTR: label slots never used yet
-  u64 kill_limit;     // thrash_kill * base_so_far (recomputed at every MAKE); 0 = off
+  u64 kill_limit;     // min(thrash_kill * base_so_far, CLOCK_LIMIT) (recomputed at every MAKE; kill 0 = off)
 };
+
+// leader-side encodings of the configuration: no decision cap = ~0, and the
+// clock stop threshold before the first MAKE = CLOCK_LIMIT
+__host__ __device__ __forceinline__ void norm_scalars(Scalars &s) {
+  if (s.max_decisions == 0) s.max_decisions = ~0ull;
+  s.kill_limit = CLOCK_LIMIT;
+}
 
 // ---------------------------------------------------------------------------
 // Exact rational scores.  den == 0 encodes +infinity.

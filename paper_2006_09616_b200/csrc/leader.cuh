@@ -457,8 +457,10 @@ struct Leader {
         }
       }
     }
-    if (s.clock > CLOCK_LIMIT) { stop(ST_CAPACITY); return false; }
-    if (s.kill_limit && s.clock > s.kill_limit) { stop(ST_THRASH); return false; }
+    if (s.clock > s.kill_limit) {                // one compare: kill_limit = min(kill x base, CLOCK_LIMIT)
+      stop(s.clock > CLOCK_LIMIT ? ST_CAPACITY : ST_THRASH);
+      return false;
+    }
     for (u32 j = 0; j < ar.y; j++) release_internal(g.par(ar.x + j));
     s.pb_top = fr.y;
     s.sp--;
@@ -509,7 +511,7 @@ struct Leader {
         u64 need = phase == PH_FREE ? free_size : g.srec(t).x;
         if (s.M + need > s.B) {
           phase = PH_FREE; free_size = need;
-          if (s.max_decisions && s.decisions >= s.max_decisions) return stop(ST_DECISION_CAP);
+          if (s.decisions >= s.max_decisions) return stop(ST_DECISION_CAP);   // 0 = none, normalised to ~0
           if (s.pool_size == 0) return stop(ST_OOM);
           return CMD_ARGMIN;
         }
@@ -533,7 +535,8 @@ struct Leader {
         for (u32 j = 0; j < pr.y; j++) if (g.rho(g.par(pr.x + j)) == 0) ok = false;   // reading C-12
         if (!ok) { if (!precond()) return CMD_DONE; continue; }
         s.base_so_far += cost;
-        s.kill_limit = (u64)s.thrash_kill * s.base_so_far;
+        s.kill_limit = s.thrash_kill && (u64)s.thrash_kill * s.base_so_far < CLOCK_LIMIT
+                           ? (u64)s.thrash_kill * s.base_so_far : CLOCK_LIMIT;
         const u32 now = (u32)(s.clock + 1);
         g.state(id) = 0;
         g.la(id) = now;
