@@ -490,6 +490,21 @@ def test_grid_engine_hub_degrees(P, oracle_mod):
     import torch
     w = models.hub_dag(20000, seed=5)
     v = LogView(w)
+    # the fixture does reach the warp walk: at most decisions a hub of degree > 32 is
+    # resident next to an evicted tensor (evicted set read off the oracle's trace)
+    nb = [[] for _ in range(v.n)]
+    for t in range(v.n):
+        for p in v.parents(t):
+            nb[p].append(t)
+            nb[t].append(p)
+    hubs = [x for x in range(v.n) if len(nb[x]) > 32]
+    _, tr = oracle_mod.replay(w, oracle_mod.HEURISTICS["dtr"], v.peak_total * 930 // 1000, max_decisions=600,
+                              trace_cap=600)
+    ev, hits = set(), 0
+    for rec in tr:
+        hits += any(x not in ev and any(q in ev for q in nb[x]) for x in hubs)
+        ev.add(int(rec["id"]))
+    assert len(hubs) >= 8 and hits > 300, (len(hubs), hits)
     specs = [dict(log=0, h=h, budget=v.peak_total * pm // 1000, max_decisions=600)
              for h in ("dtr", "dtr_eq", "abl_eqclass_ms") for pm in (930, 970)]
     assert_parity(P, oracle_mod, [w], specs, 2)
