@@ -136,6 +136,71 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &ar, u32 wslot, volati
   return sum;
 }
 
+// h_MSPS closure of ONE candidate per lane (K5, lane-parallel): e_R(t) walked
+// from t's evicted parents in DECREASING id order through a small max-heap of
+// ids.  Parents precede children in id order (the log is topologically
+// ordered), so once x is popped every later pop is < x and all copies of an id
+// pop consecutively: duplicates are dropped by comparing with the last pop,
+// and no visited set is needed.  Returns false when the frontier outgrows the
+// heap (the caller then runs the warp BFS, msps_closure).  Bytes as in
+// msps_closure: 8 per parent examined, 16 per closure member.
+constexpr u32 MSPS_HEAP = 24;
+
+template <bool SM>
+__device__ __forceinline__ bool msps_lane(const Sim<SM> &g, const uint4 &ar, u64 &sum, u64 &bytes) {
+  u32 heap[MSPS_HEAP];
+  u32 hn = 0;
+  u64 b = 0, s = 0;
+  auto push = [&](u32 x) -> bool {
+    if (hn == MSPS_HEAP) return false;
+    u32 i = hn++;
+    while (i > 0) {
+      const u32 p = (i - 1) >> 1;
+      if (heap[p] >= x) break;
+      heap[i] = heap[p];
+      i = p;
+    }
+    heap[i] = x;
+    return true;
+  };
+  auto pop = [&]() -> u32 {
+    const u32 top = heap[0], x = heap[--hn];
+    u32 i = 0;
+    for (;;) {
+      const u32 l = 2 * i + 1;
+      if (l >= hn) break;
+      const u32 c = (l + 1 < hn && heap[l + 1] > heap[l]) ? l + 1 : l;
+      if (heap[c] <= x) break;
+      heap[i] = heap[c];
+      i = c;
+    }
+    heap[i] = x;
+    return top;
+  };
+  for (u32 j = 0; j < ar.y; j++) {
+    const u32 p = g.par(ar.x + j);
+    b += 8;
+    if (is_evicted(g.state(p)) && !push(p)) return false;
+  }
+  u32 last = NONE;
+  while (hn) {
+    const u32 x = pop();
+    if (x == last) continue;
+    last = x;
+    s += g.srec(x).y;
+    b += 16;
+    const uint2 px = g.prec(x);
+    for (u32 j = 0; j < px.y; j++) {
+      const u32 p = g.par(px.x + j);
+      b += 8;
+      if (is_evicted(g.state(p)) && !push(p)) return false;
+    }
+  }
+  sum = s;
+  bytes += b;
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // Exact argmin with a fast path.  key(c) = float(num) / float(den) as monotone
 // u32 bits (0 = score 0, 0x7F800000 = +inf, 0xFFFFFFFF = no candidate).  The
@@ -595,10 +660,53 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
       break;
   }
   }
-  // H_MSPS: one warp per candidate
   const u32 nw = wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
   if (wrank >= nw) return best;
   const u32 lane = threadIdx.x & 31;
+  if (cmd.heur == H_MSPS) {
+    // one candidate per lane (msps_lane); a lane whose frontier outgrows its heap
+    // hands the candidate to the whole warp (msps_closure)
+    const u32 FULL = 0xffffffffu, n = BM ? cmd.n_ids : cmd.pool_size;
+    for (u32 base = wrank * 32; base < n; base += nw * 32) {
+      const u32 i = base + lane;
+      u32 t = NONE;
+      if (i < n) {
+        if constexpr (BM) { if (g.in_pool(i)) t = i; }
+        else t = g.pool_ids(i);
+      }
+      uint4 sr = make_uint4(0, 0, 0, 0);
+      if (t != NONE) sr = g.srec(t);
+      bool ok = true;
+      u64 sum = 0;
+      if (t != NONE && sr.w) {
+        ok = msps_lane(g, g.arec(t), sum, bytes);
+        bytes += 16;                           // adjacency record
+      }
+      if (t != NONE && ok) {
+        Cand c;
+        c.id = t; c.num = (u64)sr.y + sum; c.den = sr.x;   // (c0 + sum_{e_R}) / m
+        bytes += 16;
+        evals++;
+        cand_take(best, bk, c);
+      }
+      u32 ov = __ballot_sync(FULL, t != NONE && !ok);
+      while (ov) {
+        const u32 l = __ffs(ov) - 1;
+        ov &= ov - 1;
+        const u32 tt = __shfl_sync(FULL, t, l);
+        const u64 s2 = msps_closure(g, g.arec(tt), wrank, msps_tail + (threadIdx.x >> 5), bytes, tt, false);
+        if (lane == l) {
+          Cand c;
+          c.id = tt; c.num = (u64)sr.y + s2; c.den = sr.x;
+          bytes += 16;
+          evals++;
+          cand_take(best, bk, c);
+        }
+      }
+    }
+    return best;
+  }
+  // the e* family: one warp per candidate (ancestors and descendants)
   u32 seen = 0;
   const u32 nscan = BM ? (cmd.n_ids + 31) / 32 : cmd.pool_size;
   for (u32 w = BM ? 0 : wrank; w < nscan; w += BM ? 1 : nw) {
