@@ -519,3 +519,45 @@ def test_grid_engine_hub_degrees(P, oracle_mod):
         torch.cuda.synchronize()
         nxt = tr[D]
         assert (int(out[0]), int(out[1]), int(out[2])) == (int(nxt["num"]), int(nxt["den"]), int(nxt["id"])), h
+
+
+@pytest.mark.parametrize("width", [20, 30, 60])
+def test_percall_msps_wide_frontier(P, oracle_mod, width):
+    """MSPS with a closure frontier wider than the per-lane heap (24 ids): a
+    tensor y of `width` evicted parents (partly chained, so closures overlap) --
+    the lane walk overflows and the warp BFS takes over (width 30, 60); width 20
+    stays in the lane walk.  y is huge, so it is the first eviction and its exact
+    closure sum is in the trace; every decision must match the oracle."""
+    _msps_wide(P, oracle_mod, width)
+
+
+def _msps_wide(P, O, width):
+    B0 = 1 << 40
+    g = P.Runtime(P.HEURISTICS["msps"], budget=B0, cap_tensors=256, cap_edges=1024)
+    o = O.Runtime(O.HEURISTICS["msps"], budget=B0)
+    xs = []
+    for i in range(width):                          # x_i: cost 50, chained pairwise so closures overlap
+        ps = [xs[-1]] if xs and i % 3 else []
+        a, b = g.compute(1, 50, ps), o.compute(1, 50, ps)
+        assert a == b
+        xs.append(a[1])
+    a, b = g.compute(1 << 20, 1, xs), o.compute(1 << 20, 1, xs)   # y = f(x_0 .. x_{w-1}), huge: evicted first
+    assert a == b
+    y = a[1]
+    a, b = g.compute(1, 1, [y]), o.compute(1, 1, [y])  # z = f(y)
+    assert a == b
+    for x in xs:                                    # evict every x (pool members, outside free())
+        assert g.debug_evict(x) == o.debug_evict(x)
+    st = o.state()
+    B = int(st["M"])                                # now at the budget: the next MAKE must evict
+    g.set_budget(B)
+    o.set_budget(B)
+    for k in range(4):                              # nullary MAKEs: y stays an unlocked candidate
+        a, b = g.compute(1, 1, []), o.compute(1, 1, [])
+        assert a == b, k
+    gs, os_ = g.stats(), o.result()
+    for f in ("status", "clock", "decisions", "remats", "computations", "peak_M", "trace_hash"):
+        assert int(gs[f]) == int(os_[f]), f
+    tr = o.trace()
+    assert int(tr[0]["id"]) == y and int(tr[0]["num"]) == 1 + 50 * width   # the exact closure sum decided it
+    assert g.trace().tobytes() == tr.tobytes()
