@@ -136,27 +136,32 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &ar, u32 wslot, volati
   return sum;
 }
 
-// h_MSPS closure of ONE candidate per lane (K5, lane-parallel): e_R(t) walked
-// from t's evicted parents in DECREASING id order through a small max-heap of
-// ids.  Parents precede children in id order (the log is topologically
-// ordered), so once x is popped every later pop is < x and all copies of an id
-// pop consecutively: duplicates are dropped by comparing with the last pop,
-// and no visited set is needed.  Returns false when the frontier outgrows the
-// heap (the caller then runs the warp BFS, msps_closure).  Bytes as in
-// msps_closure: 8 per parent examined, 16 per closure member.
+// K5 closures of ONE candidate per lane (lane-parallel).  UP: e_R(t), the
+// evicted ancestors reached through evicted parents (h_MSPS), walked in
+// DECREASING id order through a small max-heap of ids; DOWN: the evicted
+// descendants reached through evicted children (the other half of the
+// directed e*(t)), in INCREASING id order through a min-heap.  Parents precede
+// children in id order (the log is topologically ordered), so after x is
+// popped every later pop lies beyond x and all copies of an id pop
+// consecutively: duplicates are dropped by comparing with the last pop, and no
+// visited set is needed.  Returns false when the frontier outgrows the heap
+// (the caller then runs the warp BFS, msps_closure).  Bytes as in
+// msps_closure: 8 per neighbour examined (+8 per children record), 16 per
+// closure member.
 constexpr u32 MSPS_HEAP = 24;
 
-template <bool SM>
-__device__ __forceinline__ bool msps_lane(const Sim<SM> &g, const uint4 &ar, u64 &sum, u64 &bytes) {
+template <bool SM, bool DOWN>
+__device__ __forceinline__ bool closure_lane(const Sim<SM> &g, u32 t, const uint4 &ar, u64 &sum, u64 &bytes) {
   u32 heap[MSPS_HEAP];
   u32 hn = 0;
   u64 b = 0, s = 0;
+  auto before = [](u32 a, u32 c) { return DOWN ? a < c : a > c; };   // heap order: first out
   auto push = [&](u32 x) -> bool {
     if (hn == MSPS_HEAP) return false;
     u32 i = hn++;
     while (i > 0) {
       const u32 p = (i - 1) >> 1;
-      if (heap[p] >= x) break;
+      if (!before(x, heap[p])) break;
       heap[i] = heap[p];
       i = p;
     }
@@ -169,19 +174,41 @@ __device__ __forceinline__ bool msps_lane(const Sim<SM> &g, const uint4 &ar, u64
     for (;;) {
       const u32 l = 2 * i + 1;
       if (l >= hn) break;
-      const u32 c = (l + 1 < hn && heap[l + 1] > heap[l]) ? l + 1 : l;
-      if (heap[c] <= x) break;
+      const u32 c = (l + 1 < hn && before(heap[l + 1], heap[l])) ? l + 1 : l;
+      if (!before(heap[c], x)) break;
       heap[i] = heap[c];
       i = c;
     }
     heap[i] = x;
     return top;
   };
-  for (u32 j = 0; j < ar.y; j++) {
-    const u32 p = g.par(ar.x + j);
-    b += 8;
-    if (is_evicted(g.state(p)) && !push(p)) return false;
-  }
+  // the evicted neighbours of x in the walk's direction
+  auto expand = [&](u32 x, u32 off, u32 cnt) -> bool {
+    if constexpr (!DOWN) {
+      for (u32 j = 0; j < cnt; j++) {
+        const u32 p = g.par(off + j);
+        b += 8;
+        if (is_evicted(g.state(p)) && !push(p)) return false;
+      }
+    } else {
+      b += 8;                                            // children record
+      if (!g.L.linked) {
+        for (u32 j = 0; j < cnt; j++) {
+          const u32 c = g.m.w(g.L.ch + off + j);
+          b += 8;
+          if (is_evicted(g.state(c)) && !push(c)) return false;
+        }
+      } else {
+        for (u32 e = g.crec(x).x; e != NONE; e = g.m.w(g.L.e_next + e)) {
+          const u32 c = g.m.w(g.L.e_child + e);
+          b += 8;
+          if (is_evicted(g.state(c)) && !push(c)) return false;
+        }
+      }
+    }
+    return true;
+  };
+  if (!(DOWN ? expand(t, ar.z, ar.w) : expand(t, ar.x, ar.y))) return false;
   u32 last = NONE;
   while (hn) {
     const u32 x = pop();
@@ -189,12 +216,9 @@ __device__ __forceinline__ bool msps_lane(const Sim<SM> &g, const uint4 &ar, u64
     last = x;
     s += g.srec(x).y;
     b += 16;
-    const uint2 px = g.prec(x);
-    for (u32 j = 0; j < px.y; j++) {
-      const u32 p = g.par(px.x + j);
-      b += 8;
-      if (is_evicted(g.state(p)) && !push(p)) return false;
-    }
+    const uint4 ax = DOWN ? g.arec(x) : make_uint4(0, 0, 0, 0);
+    const uint2 px = DOWN ? make_uint2(ax.z, ax.w) : g.prec(x);
+    if (!expand(x, px.x, px.y)) return false;
   }
   sum = s;
   bytes += b;
@@ -663,10 +687,27 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
   const u32 nw = wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
   if (wrank >= nw) return best;
   const u32 lane = threadIdx.x & 31;
-  if (cmd.heur == H_MSPS) {
-    // one candidate per lane (msps_lane); a lane whose frontier outgrows its heap
-    // hands the candidate to the whole warp (msps_closure)
+  {
+    // one candidate per lane (closure_lane: ancestors; the e* family also
+    // descendants); a lane whose frontier outgrows its heap hands the candidate
+    // to the whole warp (msps_closure)
     const u32 FULL = 0xffffffffu, n = BM ? cmd.n_ids : cmd.pool_size;
+    const bool down = cmd.heur != H_MSPS;
+    auto finish = [&](u32 t, const uint4 &sr, u64 sum) {
+      Cand c;
+      c.id = t;
+      if (cmd.heur == H_DTR_FULL) {            // (c(S) + sum_{e*(S)} c) / (size(S) * stale(S))
+        stale_score((u64)sr.y + sum, sr.x, sr.z, cmd.clock, c.num, c.den);
+      } else if (is_abl(cmd.heur)) {           // h'(s, m, e*)
+        abl_finish((u64)sr.y + sum, sr.x, sr.z, cmd, c);
+      } else {                                 // MSPS and h_e* (P:1835-1837): (c0 + sum) / m
+        c.num = (u64)sr.y + sum;
+        c.den = sr.x;
+      }
+      bytes += 16;
+      evals++;
+      cand_take(best, bk, c);
+    };
     for (u32 base = wrank * 32; base < n; base += nw * 32) {
       const u32 i = base + lane;
       u32 t = NONE;
@@ -678,67 +719,25 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
       if (t != NONE) sr = g.srec(t);
       bool ok = true;
       u64 sum = 0;
-      if (t != NONE && sr.w) {
-        ok = msps_lane(g, g.arec(t), sum, bytes);
+      if (t != NONE && sr.w) {                 // nev = 0: no evicted neighbour, the closure is empty
+        const uint4 ar = g.arec(t);
+        u64 up = 0, dn = 0, b = 0;
+        ok = closure_lane<SM, false>(g, t, ar, up, b) && (!down || closure_lane<SM, true>(g, t, ar, dn, b));
+        if (ok) { sum = up + dn; bytes += b; }
         bytes += 16;                           // adjacency record
       }
-      if (t != NONE && ok) {
-        Cand c;
-        c.id = t; c.num = (u64)sr.y + sum; c.den = sr.x;   // (c0 + sum_{e_R}) / m
-        bytes += 16;
-        evals++;
-        cand_take(best, bk, c);
-      }
+      if (t != NONE && ok) finish(t, sr, sum);
       u32 ov = __ballot_sync(FULL, t != NONE && !ok);
       while (ov) {
         const u32 l = __ffs(ov) - 1;
         ov &= ov - 1;
         const u32 tt = __shfl_sync(FULL, t, l);
-        const u64 s2 = msps_closure(g, g.arec(tt), wrank, msps_tail + (threadIdx.x >> 5), bytes, tt, false);
-        if (lane == l) {
-          Cand c;
-          c.id = tt; c.num = (u64)sr.y + s2; c.den = sr.x;
-          bytes += 16;
-          evals++;
-          cand_take(best, bk, c);
-        }
+        const u64 s2 = msps_closure(g, g.arec(tt), wrank, msps_tail + (threadIdx.x >> 5), bytes, tt, down);
+        if (lane == l) finish(tt, sr, s2);
       }
     }
     return best;
   }
-  // the e* family: one warp per candidate (ancestors and descendants)
-  u32 seen = 0;
-  const u32 nscan = BM ? (cmd.n_ids + 31) / 32 : cmd.pool_size;
-  for (u32 w = BM ? 0 : wrank; w < nscan; w += BM ? 1 : nw) {
-    u32 bits = BM ? g.pool_word(w) : 1u;
-    while (bits) {
-      const u32 b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      if (BM && (seen++ % nw) != wrank) continue;
-      const u32 t = BM ? w * 32 + b : g.pool_ids(w);
-      const uint4 sr = g.srec(t);
-      const bool down = cmd.heur != H_MSPS;
-      // nev = 0: no evicted neighbour, so the closure is empty
-      const u64 sum = sr.w ? msps_closure(g, g.arec(t), wrank, msps_tail + (threadIdx.x >> 5), bytes, t, down) : 0;
-      if (sr.w && lane == 0) bytes += 16;    // adjacency record
-      if (lane == 0) {
-        Cand c;
-        c.id = t;
-        if (cmd.heur == H_DTR_FULL) {            // (c(S) + sum_{e*(S)} c) / (size(S) * stale(S))
-          stale_score((u64)sr.y + sum, sr.x, sr.z, cmd.clock, c.num, c.den);
-        } else if (is_abl(cmd.heur)) {           // h'(s, m, e*)
-          abl_finish((u64)sr.y + sum, sr.x, sr.z, cmd, c);
-        } else {                                 // MSPS and h_e* (P:1835-1837): (c0 + sum) / m
-          c.num = (u64)sr.y + sum;
-          c.den = sr.x;
-        }
-        bytes += 16;
-        evals++;
-        cand_take(best, bk, c);
-      }
-    }
-  }
-  return best;
 }
 
 // per-call OP_SCORES (compact pool): write every pool member's score (MSPS included)
