@@ -638,54 +638,13 @@ __device__ __forceinline__ Cand intkey_cand(const Sim<SM> &g, const Cmd &cmd, u6
   return c;
 }
 
-// Score every pool member of this thread's slice; return the slice argmin and
-// its key.  rank/size: thread index in the team; wrank/wsize: warp index (MSPS).
-// WIDE: global-memory team (four candidates in flight per thread, else two).
-template <bool SM, bool BM, bool WIDE = false>
-__device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, u32 wrank, u32 wsize,
-                           volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk, u32 *slown = nullptr) {
-  Cand best = cand_none();
-  bk = KEY_NONE;
-  if (BM && rank == 0) bytes += (cmd.n_ids + 7) / 8;     // the pool bitmap
-  constexpr u32 K = WIDE ? 4 : 2;
-  if constexpr (!SM && BM) {
-    switch (cmd.heur) {
-      case H_DTR: score_bm<H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_DTR_EQ: score_bm<H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_LRU: score_bm<H_LRU, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_SIZE: score_bm<H_SIZE, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_LOCAL: score_bm<H_LOCAL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_RANDOM: score_bm<H_RANDOM, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      default:
-        if (is_abl(cmd.heur) && abl_c(cmd.heur) != ABL_ESTAR) {
-          score_bm<H_ABL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown);
-          return best;
-        }
-        break;
-    }
-  } else {
-  if (g.L.pool_key) {
-    const u64 kmin = team_intkey_min(g, cmd, rank, size, bytes, evals);
-    if (kmin != ~0ull) { best = intkey_cand(g, cmd, kmin); bk = cand_key(best, true); }
-    return best;
-  }
-  switch (cmd.heur) {
-    case H_DTR: score_loop<SM, H_DTR, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_DTR_EQ: score_loop<SM, H_DTR_EQ, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_LRU: score_loop<SM, H_LRU, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_SIZE: score_loop<SM, H_SIZE, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_LOCAL: score_loop<SM, H_LOCAL, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    case H_RANDOM: score_loop<SM, H_RANDOM, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
-    default:
-      if (is_abl(cmd.heur) && abl_c(cmd.heur) != ABL_ESTAR) {
-        score_loop<SM, H_ABL, 2>(g, cmd, rank, size, best, bk, bytes, evals);
-        return best;
-      }
-      break;
-  }
-  }
+// K5 pass: h_MSPS and the e* family (one candidate per lane, warp BFS on
+// frontier overflow).
+template <bool SM, bool BM>
+__device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u32 wrank, u32 wsize,
+                                             volatile u32 *msps_tail, u64 &bytes, u64 &evals, Cand &best, u32 &bk) {
   const u32 nw = wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
-  if (wrank >= nw) return best;
+  if (wrank >= nw) return;
   const u32 lane = threadIdx.x & 31;
   {
     // one candidate per lane (closure_lane: ancestors; the e* family also
@@ -736,8 +695,62 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
         if (lane == l) finish(tt, sr, s2);
       }
     }
+  }
+}
+
+// Score every pool member of this thread's slice; return the slice argmin and
+// its key.  rank/size: thread index in the team; wrank/wsize: warp index (MSPS).
+// WIDE: global-memory team (four candidates in flight per thread, else two).
+template <bool SM, bool BM, bool WIDE = false, bool CL = true>
+__device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, u32 wrank, u32 wsize,
+                           volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk, u32 *slown = nullptr) {
+  Cand best = cand_none();
+  bk = KEY_NONE;
+  if (BM && rank == 0) bytes += (cmd.n_ids + 7) / 8;     // the pool bitmap
+  if constexpr (CL) {   // CL = false: a kernel built for batches without closure heuristics (dtr.cu)
+    if (uses_closure(cmd.heur)) {
+      team_closure<SM, BM>(g, cmd, wrank, wsize, msps_tail, bytes, evals, best, bk);
+      return best;
+    }
+  }
+  constexpr u32 K = WIDE ? 4 : 2;
+  if constexpr (!SM && BM) {
+    switch (cmd.heur) {
+      case H_DTR: score_bm<H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_DTR_EQ: score_bm<H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_LRU: score_bm<H_LRU, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_SIZE: score_bm<H_SIZE, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_LOCAL: score_bm<H_LOCAL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_RANDOM: score_bm<H_RANDOM, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      default:
+        if (is_abl(cmd.heur) && abl_c(cmd.heur) != ABL_ESTAR) {
+          score_bm<H_ABL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown);
+          return best;
+        }
+        break;
+    }
+  } else {
+  if (g.L.pool_key) {
+    const u64 kmin = team_intkey_min(g, cmd, rank, size, bytes, evals);
+    if (kmin != ~0ull) { best = intkey_cand(g, cmd, kmin); bk = cand_key(best, true); }
     return best;
   }
+  switch (cmd.heur) {
+    case H_DTR: score_loop<SM, H_DTR, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_DTR_EQ: score_loop<SM, H_DTR_EQ, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_LRU: score_loop<SM, H_LRU, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_SIZE: score_loop<SM, H_SIZE, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_LOCAL: score_loop<SM, H_LOCAL, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    case H_RANDOM: score_loop<SM, H_RANDOM, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;
+    default:
+      if (is_abl(cmd.heur) && abl_c(cmd.heur) != ABL_ESTAR) {
+        score_loop<SM, H_ABL, 2>(g, cmd, rank, size, best, bk, bytes, evals);
+        return best;
+      }
+      break;
+  }
+  }
+  return best;
 }
 
 // per-call OP_SCORES (compact pool): write every pool member's score (MSPS included)
