@@ -23,6 +23,9 @@ print(f"LIB={os.environ.get('DTR_LIB', 'libdtr.so')} whole batch {e0.elapsed_tim
 res.sort(reverse=True)
 for ms, h, B, d, rm, st in res[:12]:
     print(f"{ms:8.3f} ms  {h:7s} B={B:9d} dec={d:6d} remats={rm:6d} st={st} us/dec={1000*ms/max(d,1):.2f}")
+for name in names.values():                      # the slowest cells of each heuristic
+    for ms, h, B, d, rm, st in [r for r in res if r[1] == name][:2]:
+        print(f"  top {h:7s} {ms:8.3f} ms B={B:9d} dec={d:6d} remats={rm:6d} st={st} us/dec={1000*ms/max(d,1):.2f}")
 tot = {}
 for ms, h, B, d, rm, st in res:
     t = tot.setdefault(h, [0, 0]); t[0] += ms; t[1] += d
