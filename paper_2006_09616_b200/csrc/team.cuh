@@ -297,71 +297,17 @@ __device__ __forceinline__ Cand warp_argmin_fast(const Cand &c, u32 k, bool ik =
   return b;
 }
 
-// h'(s, m, c) = c / (m * s) with ablated measures = 1 (P:2527-2536, reading C-23)
-__device__ __forceinline__ void abl_finish(u64 c, u32 mem, u32 la, const Cmd &cmd, Cand &out) {
-  const u32 code = cmd.heur - H_ABL;
-  const u32 m = (code & 2) ? mem : 1u;
-  if (code & 1) stale_score(c, m, la, cmd.clock, out.num, out.den);
-  else { out.num = c; out.den = m; }
-}
-
-// per-heuristic score of pool member t
-template <bool SM, int H>
-__device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t, Cand &c, u64 &bytes) {
-  c.id = t;
-  if constexpr (H == H_DTR || H == H_DTR_EQ) {
-    const uint4 sr = g.srec(t);
-    u64 sum = 0;
-    u32 L = sr.z;
-    bytes += 16;                  // score record
-    if (sr.w) {                   // evicted neighbours: walk them
-      nbr_components<SM, H == H_DTR_EQ>(g, t, g.arec(t), sum, L, bytes);
-      bytes += 16;                // adjacency record
-    }
-    stale_score((u64)sr.y + sum, sr.x, L, cmd.clock, c.num, c.den);
-  } else if constexpr (H == H_LRU) {
-    stale_score(1, 1, g.la(t), cmd.clock, c.num, c.den);
-    bytes += 4;
-  } else if constexpr (H == H_SIZE) {
-    c.num = 1; c.den = g.srec(t).x;
-    bytes += 4;
-  } else if constexpr (H == H_LOCAL) {
-    const uint4 sr = g.srec(t);
-    stale_score((u64)sr.y, sr.x, sr.z, cmd.clock, c.num, c.den);
-    bytes += 12;
-  } else if constexpr (H == H_ABL) {           // h'(s, m, c) with c in {EqClass, local, no}
-    const uint4 sr = g.srec(t);
-    const u32 cc = abl_c(cmd.heur);
-    u64 num = 1;
-    if (cc == ABL_EQCLASS) {                   // c(t) + the distinct adjacent sets' costs (P:2286-2293)
-      u64 sum = 0;
-      u32 L = 0;
-      if (sr.w) {
-        nbr_components<SM, true>(g, t, g.arec(t), sum, L, bytes);
-        bytes += 16;
-      }
-      num = (u64)sr.y + sum;
-    } else if (cc == ABL_LOCAL) {
-      num = sr.y;
-    }
-    abl_finish(num, sr.x, sr.z, cmd, c);
-    bytes += 16;
-  } else {
-    c.num = splitmix64(cmd.seed ^ (cmd.decisions << 32) ^ (u64)t); c.den = 1;
-    bytes += 4;
-  }
-}
-
-// One candidate with evicted neighbours per lane (whole-GPU team, phase 2), in
-// fixed unrolled phases so every load of a phase is independent (in-order
-// issue would otherwise pay one memory latency per neighbour): neighbour ids
-// -> their states (-> union-find roots) -> distinct component records.  Only
-// for deg(t) <= NB; returns the sum of the distinct adjacent components' cost
-// and the max of their max la with la(t).
+// E(t) aggregation for one candidate with evicted neighbours, in fixed
+// unrolled phases so every load of a phase is independent (in-order issue
+// would otherwise pay one memory latency per neighbour): neighbour ids ->
+// their states (-> union-find roots) -> distinct component records.  Only for
+// deg(t) <= NB and CSR children (not the per-call linked lists); returns the
+// sum of the distinct adjacent components' cost and the max of their max la
+// with la(t).  Used per lane by the whole-GPU team's phase 2 and by score_h.
 constexpr u32 NB = 8;
 
-template <bool UF>
-__device__ __forceinline__ void nbr_components_phased(const Sim<false> &g, const uint4 &sr, const uint4 &ar,
+template <bool SM, bool UF>
+__device__ __forceinline__ void nbr_components_phased(const Sim<SM> &g, const uint4 &sr, const uint4 &ar,
                                                       u64 &sum, u32 &L, u64 &bytes) {
   const u32 deg = ar.y + ar.w;
   u32 q[NB], lab[NB];
@@ -408,6 +354,68 @@ __device__ __forceinline__ void nbr_components_phased(const Sim<false> &g, const
   sum = s;
   L = mx;
   bytes += 16 + 8ull * deg + 12ull * nd;     // adjacency record, ids + states, components
+}
+
+// h'(s, m, c) = c / (m * s) with ablated measures = 1 (P:2527-2536, reading C-23)
+__device__ __forceinline__ void abl_finish(u64 c, u32 mem, u32 la, const Cmd &cmd, Cand &out) {
+  const u32 code = cmd.heur - H_ABL;
+  const u32 m = (code & 2) ? mem : 1u;
+  if (code & 1) stale_score(c, m, la, cmd.clock, out.num, out.den);
+  else { out.num = c; out.den = m; }
+}
+
+// per-heuristic score of pool member t
+template <bool SM, int H>
+__device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t, Cand &c, u64 &bytes) {
+  c.id = t;
+  if constexpr (H == H_DTR || H == H_DTR_EQ) {
+    const uint4 sr = g.srec(t);
+    u64 sum = 0;
+    u32 L = sr.z;
+    bytes += 16;                  // score record
+    if (sr.w) {                   // evicted neighbours: walk them
+      const uint4 ar = g.arec(t);
+      // h_DTR: phased gathers (measured -7 % on the bench's h_DTR cells); h_DTR_eq's
+      // union-find finds are chains, where the sequential walk measured faster
+      if (H == H_DTR && !g.L.linked && ar.y + ar.w <= NB) {
+        nbr_components_phased<SM, false>(g, sr, ar, sum, L, bytes);   // counts the adjacency record
+      } else {
+        nbr_components<SM, H == H_DTR_EQ>(g, t, ar, sum, L, bytes);
+        bytes += 16;              // adjacency record
+      }
+    }
+    stale_score((u64)sr.y + sum, sr.x, L, cmd.clock, c.num, c.den);
+  } else if constexpr (H == H_LRU) {
+    stale_score(1, 1, g.la(t), cmd.clock, c.num, c.den);
+    bytes += 4;
+  } else if constexpr (H == H_SIZE) {
+    c.num = 1; c.den = g.srec(t).x;
+    bytes += 4;
+  } else if constexpr (H == H_LOCAL) {
+    const uint4 sr = g.srec(t);
+    stale_score((u64)sr.y, sr.x, sr.z, cmd.clock, c.num, c.den);
+    bytes += 12;
+  } else if constexpr (H == H_ABL) {           // h'(s, m, c) with c in {EqClass, local, no}
+    const uint4 sr = g.srec(t);
+    const u32 cc = abl_c(cmd.heur);
+    u64 num = 1;
+    if (cc == ABL_EQCLASS) {                   // c(t) + the distinct adjacent sets' costs (P:2286-2293)
+      u64 sum = 0;
+      u32 L = 0;
+      if (sr.w) {
+        nbr_components<SM, true>(g, t, g.arec(t), sum, L, bytes);
+        bytes += 16;
+      }
+      num = (u64)sr.y + sum;
+    } else if (cc == ABL_LOCAL) {
+      num = sr.y;
+    }
+    abl_finish(num, sr.x, sr.z, cmd, c);
+    bytes += 16;
+  } else {
+    c.num = splitmix64(cmd.seed ^ (cmd.decisions << 32) ^ (u64)t); c.den = 1;
+    bytes += 4;
+  }
 }
 
 // Warp-cooperative E(t) aggregation for ONE candidate t with evicted neighbours
@@ -583,7 +591,7 @@ __device__ __forceinline__ void score_bm(const Sim<false> &g, const Cmd &cmd, u3
       if (t != NONE && !big) {
         u64 sum;
         u32 L;
-        nbr_components_phased<UF>(g, sr, ar, sum, L, bytes);
+        nbr_components_phased<false, UF>(g, sr, ar, sum, L, bytes);
         finish(t, sr, sum, L);
       }
       u32 bm = __ballot_sync(FULL, big);
