@@ -135,6 +135,10 @@ typedef struct {
  * simulation (one large run, K7: cooperative persistent grid). */
 #define DTR_ENGINE_CTA 1
 #define DTR_ENGINE_GRID 2
+/* Automatic engine choice (dtr_replay_batch_host with engine 0, and the
+ * sweep's rank split): logs with at least this many tensors replay on the
+ * whole-GPU engine. */
+#define DTR_GRID_MIN_TENSORS 65536u
 
 const char *dtr_strerror(int code);
 const char *dtr_last_cuda_error(void);

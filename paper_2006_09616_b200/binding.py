@@ -32,6 +32,7 @@ for _c in ABL_C:
         for _s in (0, 1):
             HEURISTICS[f"abl_{_c}_{'m' if _m else 'x'}{'s' if _s else 'x'}"] = abl_id(_c, _m, _s)
 ENGINE_CTA, ENGINE_GRID = 1, 2
+GRID_MIN_TENSORS = 65536   # include/dtr.h DTR_GRID_MIN_TENSORS: logs this large replay on the whole-GPU engine
 DEALLOC = {"v2": 0, "v1": 1, "eager": 2, "ignore": 3}
 STATUS_NAMES = {0: "ok", 1: "inval", 2: "precond", 3: "oom", 4: "thrash_killed", 5: "capacity",
                 6: "state", 7: "cuda", 8: "decision_cap"}

@@ -43,7 +43,7 @@
 // [0] leader resume cycles, [1] warp-team score cycles, [2] warp reduce cycles,
 // [3] warp-team decisions, [4] cta-team cycles, [5] cta-team decisions, [6] init cycles,
 // [8/9] record_and_evict cycles/calls, [10/11] complete_top, [12/13] push, [14] resume loop iterations
-__device__ unsigned long long g_prof[16];
+static __device__ unsigned long long g_prof[16];
 #define PROF_T(x) unsigned long long x = clock64()
 #define PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
 #else
@@ -103,14 +103,17 @@ struct Lay {
   u32 mem_next, comp, comp_head, bfs_q, stamp;         // h_DTR (comp rec: {cost lo, cost hi, maxla, size})
   u32 mem_prev, comp_free;                             // h_DTR: member lists are doubly linked; free label slots
   u32 node_of, uf, uf_size, uf_cap;                    // h_DTR_eq (uf rec: {cost lo, cost hi, maxla, parent})
-  u32 msps_bm, msps_q, msps_words, msps_warps;         // h_MSPS per-warp scratch
+  u32 msps_bm, msps_q, msps_words, msps_warps;         // closure BFS scratch: msps_warps slots
+  u32 msps_lock;                                       // grid: slot locks (0 = CTA: slot = warp)
   u32 e_next, e_child;                                 // linked children (per-call)
   u32 slowq;                                           // whole-GPU team: candidates with nev > 0
   u32 words;                                           // total
 };
 
 // Sizes the workspace (host) and places it (device).  Returns false when the
-// layout does not fit 32-bit word offsets.
+// layout does not fit 32-bit word offsets (the caller reports DTR_E_CAPACITY).
+// msps_warps: closure-BFS scratch slots (one per scoring warp on a CTA; on the
+// whole-GPU engine a bounded number of slots that warps lock, grid_closure_slots).
 __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 linked, u32 msps_warps,
                                             u32 grid = 0) {
   u64 o = 0;
@@ -135,7 +138,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
   L.mem_next = L.comp = L.comp_head = L.bfs_q = L.stamp = 0;
   L.mem_prev = L.comp_free = 0;
   L.node_of = L.uf = L.uf_size = L.uf_cap = 0;
-  L.msps_bm = L.msps_q = L.msps_words = L.msps_warps = 0;
+  L.msps_bm = L.msps_q = L.msps_words = L.msps_warps = L.msps_lock = 0;
   L.e_next = L.e_child = 0;
   if (heur == H_DTR) {
     L.mem_next = take(n1);
@@ -155,6 +158,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
     L.msps_words = (u32)((n1 + 31) / 32);
     L.msps_bm = take((u64)L.msps_words * msps_warps);
     L.msps_q = take(n1 * msps_warps);
+    if (grid) L.msps_lock = take(msps_warps);
   }
   if (linked) {
     L.e_next = take(e1);
@@ -163,6 +167,16 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
   L.slowq = grid ? take(n1) : 0;
   L.words = (u32)o;
   return o < 0xFFFFFFF0ull;
+}
+
+// Closure-BFS scratch slots of the whole-GPU engine: each slot is a visited
+// bitmap + queue of n + 1 words, so the slots are bounded to ~64 Mi words
+// (256 MiB) in total; the lane-parallel walk needs no scratch and the BFS is
+// only the fallback for frontiers wider than the lane heap.
+__host__ __device__ inline u32 grid_closure_slots(u32 n) {
+  const u64 per = (u64)n + 1 + ((u64)n + 32) / 32;
+  u64 k = (64ull << 20) / per;
+  return k < 1 ? 1u : (k > 1024 ? 1024u : (u32)k);
 }
 
 // ---------------------------------------------------------------------------

@@ -651,7 +651,10 @@ __device__ __forceinline__ Cand intkey_cand(const Sim<SM> &g, const Cmd &cmd, u6
 template <bool SM, bool BM>
 __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u32 wrank, u32 wsize,
                                              volatile u32 *msps_tail, u64 &bytes, u64 &evals, Cand &best, u32 &bk) {
-  const u32 nw = wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
+  // CTA: one BFS slot per scoring warp; whole GPU (msps_lock): every warp walks
+  // lanes, and the rare BFS fallback locks one of the bounded slots
+  const bool locked = g.L.msps_lock != 0;
+  const u32 nw = locked || wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
   if (wrank >= nw) return;
   const u32 lane = threadIdx.x & 31;
   {
@@ -699,7 +702,18 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
         const u32 l = __ffs(ov) - 1;
         ov &= ov - 1;
         const u32 tt = __shfl_sync(FULL, t, l);
-        const u64 s2 = msps_closure(g, g.arec(tt), wrank, msps_tail + (threadIdx.x >> 5), bytes, tt, down);
+        u32 slot = wrank;
+        if (locked) {                            // acquire a free slot (its holder always finishes)
+          if (lane == 0) {
+            u32 k = wrank % g.L.msps_warps;
+            while (atomicCAS(&g.m.w(g.L.msps_lock + k), 0u, 1u) != 0u) k = k + 1 == g.L.msps_warps ? 0 : k + 1;
+            __threadfence();
+            slot = k;
+          }
+          slot = __shfl_sync(FULL, slot, 0);
+        }
+        const u64 s2 = msps_closure(g, g.arec(tt), slot, msps_tail + (threadIdx.x >> 5), bytes, tt, down);
+        if (locked && lane == 0) { __threadfence(); atomicExch(&g.m.w(g.L.msps_lock + slot), 0u); }
         if (lane == l) finish(tt, sr, s2);
       }
     }

@@ -17,11 +17,10 @@ from __future__ import annotations
 
 import numpy as np
 
-from .binding import (DeviceBatch, RESULT_DTYPE, ENGINE_CTA, ENGINE_GRID, HEURISTICS)
+from .binding import (DeviceBatch, RESULT_DTYPE, ENGINE_CTA, ENGINE_GRID, HEURISTICS, GRID_MIN_TENSORS)
 
 # relative per-decision cost of a heuristic's score (MSPS walks closures)
 HEUR_WEIGHT = {0: 3.0, 1: 3.0, 2: 1.0, 3: 1.0, 4: 6.0, 5: 1.5, 6: 1.0, 7: 8.0, 8: 8.0}
-GRID_MIN_TENSORS = 65536   # logs at least this large replay on the whole-GPU engine
 
 
 def make_cells(log_views, permilles, heuristics, thrash_kill=16, max_decisions=0):
