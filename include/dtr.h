@@ -97,7 +97,7 @@ typedef struct {
   uint64_t den;
 } dtr_evict_rec;
 
-/* Per-run result row (88 B).  `status` is DTR_OK or the code that stopped the
+/* Per-run result row (96 B).  `status` is DTR_OK or the code that stopped the
  * run; counters are the state at the stop.  trace_hash = FNV-1a-64 folded over
  * (clock, id, num, den) of every decision, one 64-bit word at a time:
  * h = 14695981039346656037; for w in words: h = (h ^ w) * 1099511628211. */
@@ -115,6 +115,8 @@ typedef struct {
   uint64_t trace_hash;
   uint64_t cand_evals;     /* pool members scored over all decisions (batch engines) */
   uint64_t score_bytes;    /* algorithmic bytes those score passes read (DESIGN.md Roofline) */
+  uint64_t wall_ns;        /* device time of this run, first to last instruction (%globaltimer, ns;
+                              batch engines and the adversary; 0 for the per-call runtime) */
 } dtr_result;
 
 /* One simulation of a sweep (64 B). */

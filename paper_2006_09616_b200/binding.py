@@ -41,13 +41,13 @@ TRACE_DTYPE = np.dtype([("clock", "<u8"), ("id", "<u4"), ("pad", "<u4"), ("num",
 RESULT_DTYPE = np.dtype([("cell_id", "<u4"), ("status", "<u4"), ("records_done", "<u4"), ("n_trace", "<u4"),
                          ("clock", "<u8"), ("base", "<u8"), ("decisions", "<u8"), ("remats", "<u8"),
                          ("computations", "<u8"), ("peak_M", "<u8"), ("trace_hash", "<u8"),
-                         ("cand_evals", "<u8"), ("score_bytes", "<u8")])
+                         ("cand_evals", "<u8"), ("score_bytes", "<u8"), ("wall_ns", "<u8")])
 CELL_DTYPE = np.dtype([("log_offset", "<u8"), ("budget", "<u8"), ("seed", "<u8"), ("max_decisions", "<u8"),
                        ("trace_offset", "<u8"), ("trace_cap", "<u8"), ("heuristic", "<u4"),
                        ("thrash_kill", "<u4"), ("cell_id", "<u4"), ("dealloc", "<u4")])
 ADV_DTYPE = np.dtype([("n", "<u4"), ("budget", "<u4"), ("heuristic", "<u4"), ("cell_id", "<u4"),
                       ("seed", "<u8"), ("trace_offset", "<u8"), ("trace_cap", "<u4"), ("reserved", "<u4")])
-assert TRACE_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 88 and CELL_DTYPE.itemsize == 64
+assert TRACE_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 96 and CELL_DTYPE.itemsize == 64
 assert ADV_DTYPE.itemsize == 40
 
 # every symbol include/dtr.h declares

@@ -100,7 +100,7 @@ struct Lay {
   u32 n, E, heur, linked, track_nev;
   u32 srec, arec, par, ch, state, rho, ell, pool_bm, pool_words, pool_ids, pool_pos, fr, pb;
   u32 pool_key;                                        // compact list, size/LRU: u64 key per slot (0 = none)
-  u32 mem_next, comp, comp_head, bfs_q, stamp;         // h_DTR (comp rec: {cost lo, cost hi, maxla, size})
+  u32 mem_next, comp, comp_head, bfs_q, stamp;         // h_DTR (comp rec: {cost, nmax, maxla, size})
   u32 mem_prev, comp_free;                             // h_DTR: member lists are doubly linked; free label slots
   u32 node_of, uf, uf_size, uf_cap;                    // h_DTR_eq (uf rec: {cost lo, cost hi, maxla, parent})
   u32 msps_bm, msps_q, msps_words, msps_warps;         // closure BFS scratch: msps_warps slots
@@ -149,7 +149,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
     L.bfs_q = take(n1);
     L.stamp = take(n1);
   } else if (uses_uf(heur)) {
-    L.uf_cap = n + 64;
+    L.uf_cap = 2 * n + 64;                             // compaction at most once per n + 64 evictions
     L.node_of = take(n1);
     L.uf = take(4 * (u64)L.uf_cap);
     L.uf_size = take(L.uf_cap);

@@ -52,6 +52,7 @@ __device__ void run_adversary(const dtr_adversary &run, u32 *gbase, dtr_result *
                               dtr_evict_rec *trace, AdvShared &sh) {
   const u32 tid = threadIdx.x;
   const u32 N = run.n, B = run.budget;
+  const u64 t_start = gtimer();
   Sim<SM> g;
   g.m.gbase = gbase;
   AdvLay A;
@@ -160,7 +161,7 @@ __device__ void run_adversary(const dtr_adversary &run, u32 *gbase, dtr_result *
     __syncthreads();
   }
   block_sum2(bytes, evals, sh.red);
-  if (tid == 0) write_row(*row, L.s, bytes, evals);
+  if (tid == 0) write_row(*row, L.s, bytes, evals, t_start);
 }
 
 __global__ void __launch_bounds__(CTA_THREADS, 1) adversary_engine(const dtr_adversary *runs, u32 n_runs, char *ws,

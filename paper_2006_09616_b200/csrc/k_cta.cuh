@@ -43,6 +43,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   g.m.gbase = gbase;
   make_layout(g.L, logw[2], logw[3], cell.heuristic, 0, CTA_THREADS / 32);
   PROF_T(ti0);
+  const u64 t_start = gtimer();
   init_sim(g, logw, tid, blockDim.x, true, sh.scan, CtaSync());
   PROF_T(ti1);
   if (tid == 0) PROF_ADD(6, ti1 - ti0);
@@ -90,7 +91,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       PROF_T(t6);
       if (lane == 0) { res = best; have = true; PROF_ADD(4, t6 - t5); PROF_ADD(5, 1); }
     }
-    if (lane == 0) write_row(*row, L.s, 0, 0);
+    if (lane == 0) write_row(*row, L.s, 0, 0, t_start);
   } else {
     for (;;) {
       __syncthreads();

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
                                                             dtr_evict_rec *trace) {
   __shared__ GridShared sh;
   cg::grid_group grid = cg::this_grid();
+  const u64 t_start = gtimer();
   const u32 tid = threadIdx.x;
   Cmd *gcmd = (Cmd *)ws;
   u64 *gstats = (u64 *)(ws + 64);   // [bytes, evals]
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
   if (tid == 0) { atomicAdd(&gstats[0], bytes); atomicAdd(&gstats[1], evals); }
   grid.sync();
   if (rank == 0) {
-    write_row(rows[ci], L.s, __ldcg(&gstats[0]), __ldcg(&gstats[1]));
+    write_row(rows[ci], L.s, __ldcg(&gstats[0]), __ldcg(&gstats[1]), t_start);
     *(Scalars *)(ws + WS_SCALARS) = L.s;   // kept for dtr_pool_argmin
   }
 }

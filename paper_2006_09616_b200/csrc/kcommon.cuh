@@ -152,7 +152,14 @@ static __device__ void init_scalars(Scalars &s, const dtr_cell &cell) {
   norm_scalars(s);
 }
 
-static __device__ void write_row(dtr_result &r, const Scalars &s, u64 bytes, u64 evals) {
+static __device__ __forceinline__ u64 gtimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// t0: gtimer() at the start of the run (0: wall_ns = 0)
+static __device__ void write_row(dtr_result &r, const Scalars &s, u64 bytes, u64 evals, u64 t0 = 0) {
   dtr_result x;
   x.cell_id = s.cell_id;
   x.status = s.status;
@@ -167,6 +174,7 @@ static __device__ void write_row(dtr_result &r, const Scalars &s, u64 bytes, u64
   x.trace_hash = s.trace_hash;
   x.cand_evals = evals;
   x.score_bytes = bytes;
+  x.wall_ns = t0 ? gtimer() - t0 : 0;
   r = x;
 }
 

@@ -9,9 +9,9 @@
 //                                    P:1236-1250
 //   exact evicted components (h_DTR: E(t) of P:63-68 is the union of the
 //   components adjacent to t; maintained incrementally -- merge the smaller
-//   into the larger on evict, split by BFS on rematerialization).  A
-//   component's label is the id of one of its members, so labels never need a
-//   free list: a newly evicted t starts component t.
+//   into the larger on evict; on rematerialization, interleaved searches from
+//   t's evicted neighbours split off only the smaller pieces).  Labels are
+//   slots of the component table, recycled through a free stack.
 //
 // resume() runs until free() needs an eviction decision (returns CMD_ARGMIN;
 // the team computes it and the next resume() applies it) or the op range is
@@ -169,7 +169,10 @@ struct Leader {
   // ------------------------------------------------------------- exact components
   // Component labels are slots of the component table, taken from a free stack
   // (or the never-used range) and returned when a component is absorbed or
-  // dissolved; member lists are doubly linked.
+  // dissolved; member lists are doubly linked.  Record {cost, nmax, maxla,
+  // size}: cost = sum of the members' c0 (< 2^32, reading C-14), maxla = the
+  // max encoded la over the members and nmax = how many members hold it, so
+  // removing a holder forces a rescan only when it was the last one.
   __device__ __forceinline__ u32 comp_alloc() {
     if (s.comp_top) return g.m.w(g.L.comp_free + --s.comp_top);
     return s.comp_fresh++;
@@ -186,8 +189,9 @@ struct Leader {
     g.m.w(g.L.mem_next + last) = ha;
     if (ha != NONE) g.m.w(g.L.mem_prev + ha) = last;
     g.m.w(g.L.comp_head + a) = g.m.w(g.L.comp_head + b);
-    u64 cost = mk64(ca.x, ca.y) + mk64(cb.x, cb.y);
-    g.comp(a) = make_uint4((u32)cost, (u32)(cost >> 32), ca.z > cb.z ? ca.z : cb.z, ca.w + cb.w);
+    const u32 mx = ca.z > cb.z ? ca.z : cb.z;
+    const u32 nm = (ca.z == mx ? ca.y : 0u) + (cb.z == mx ? cb.y : 0u);
+    g.comp(a) = make_uint4(ca.x + cb.x, nm, mx, ca.w + cb.w);
     comp_release(b);
     return a;
   }
@@ -196,7 +200,7 @@ struct Leader {
   // (fused: every neighbour's nev += 1)
   __device__ __forceinline__ void evict_exact(u32 t, const uint4 &sr, const uint4 &ar) {
     const u32 c0 = comp_alloc();
-    g.comp(c0) = make_uint4(sr.y, 0, sr.z, 1);
+    g.comp(c0) = make_uint4(sr.y, 1, sr.z, 1);
     g.m.w(g.L.comp_head + c0) = t;
     g.m.w(g.L.mem_next + t) = NONE;
     g.m.w(g.L.mem_prev + t) = NONE;
@@ -211,46 +215,154 @@ struct Leader {
     });
   }
 
-  // max last_access over the members of c (la encoded, 0 = -inf)
-  __device__ __forceinline__ u32 comp_rescan_maxla(u32 c) {
-    u32 mx = 0;
+  // {max la, number of holders} over the members of c (la encoded, 0 = -inf)
+  __device__ __forceinline__ uint2 comp_rescan_maxla(u32 c) {
+    u32 mx = 0, nm = 0;
     for (u32 x = g.m.w(g.L.comp_head + c); x != NONE; x = g.m.w(g.L.mem_next + x)) {
       const u32 l = g.la(x);
-      mx = l > mx ? l : mx;
+      if (l > mx) { mx = l; nm = 1; } else if (l == mx) nm++;
     }
-    return mx;
+    return make_uint2(mx, nm);
   }
 
-  // t (formerly in component c, with k = nev(t) evicted neighbours) has just
-  // stopped being evicted.  k = 0: c was {t}.  k = 1: t was a leaf of c, which
-  // stays connected -- unlink t, subtract its cost, rescan the max la only if
-  // t held it.  k >= 2: relabel c \ {t} by BFS from t's evicted neighbours;
-  // each BFS tree becomes a component with a fresh label.
-  __device__ __forceinline__ void remat_exact(u32 t, const uint4 &ar, u32 c) {
+  __device__ __forceinline__ void list_unlink(u32 c, u32 x) {
+    const u32 p = g.m.w(g.L.mem_prev + x), nx = g.m.w(g.L.mem_next + x);
+    if (p != NONE) g.m.w(g.L.mem_next + p) = nx;
+    else g.m.w(g.L.comp_head + c) = nx;
+    if (nx != NONE) g.m.w(g.L.mem_prev + nx) = p;
+  }
+
+  // BFS visit stamps: (epoch << 5) | search id; the epoch wraps after 2^27 splits
+  __device__ __forceinline__ u32 next_epoch() {
+    if (s.epoch == (1u << 27) - 1) {
+      for (u32 q = 0; q < s.n_alloc; q++) g.m.w(g.L.stamp + q) = 0;
+      s.epoch = 0;
+    }
+    return (++s.epoch) << 5;
+  }
+
+  // Removing t from its component c may split c \ {t} into up to k = nev(t)
+  // pieces, one per evicted neighbour of t at most.  k = 0: c was {t}.  k = 1:
+  // t was a leaf, c \ {t} stays connected.  k >= 2: one search per evicted
+  // neighbour, expanded one node at a time in turn; searches that meet are
+  // the same piece.  A search group whose queues run dry has found a whole
+  // piece; the run stops as soon as at most one group is still growing --
+  // that one is the rest of c and keeps its label and member list, so only
+  // the smaller pieces are ever walked (all groups meeting = no split, the
+  // common case when t's evicted neighbours are linked around it).
+  static constexpr u32 KS = 32;
+  __device__ void remat_exact(u32 t, const uint4 &ar, u32 c) {
     const uint4 cc = g.comp(c);
     if (cc.w == 1) { comp_release(c); return; }
-    if (g.nev(t) == 1) {
-      const u32 p = g.m.w(g.L.mem_prev + t), nx = g.m.w(g.L.mem_next + t);
-      if (p != NONE) g.m.w(g.L.mem_next + p) = nx;
-      else g.m.w(g.L.comp_head + c) = nx;
-      if (nx != NONE) g.m.w(g.L.mem_prev + nx) = p;
-      const uint4 st = g.srec(t);
-      const u64 cost = mk64(cc.x, cc.y) - st.y;
-      const u32 mx = st.z == cc.z ? comp_rescan_maxla(c) : cc.z;
-      g.comp(c) = make_uint4((u32)cost, (u32)(cost >> 32), mx, cc.w - 1);
-      return;
+    const uint4 st = g.srec(t);
+    list_unlink(c, t);
+    const u32 k = g.nev(t);
+    if (k > KS) { split_all(t, ar, c); return; }
+    u32 cost = cc.x - st.y, size = cc.w - 1, nmax = cc.y - (st.z == cc.z ? 1u : 0u);
+    if (k >= 2) {
+      u32 first[KS], cur[KS], last[KS], cst[KS], sz[KS], nmc[KS], up[KS];
+      u32 nq = 0;
+      const u32 ep = next_epoch();
+      const u32 VN = g.L.bfs_q;                          // visit lists (vnext)
+      auto seed = [&](u32 q) {
+        const u32 i = nq++;
+        const uint4 sq = g.srec(q);
+        g.m.w(g.L.stamp + q) = ep | i;
+        g.m.w(VN + q) = NONE;
+        first[i] = cur[i] = last[i] = q;
+        cst[i] = sq.y; sz[i] = 1; nmc[i] = sq.z == cc.z ? 1u : 0u; up[i] = i;
+      };
+      g.for_each_nbr(t, ar, [&](u32 q) { if (is_evicted(g.state(q))) seed(q); });
+      auto root = [&](u32 i) { while (up[i] != i) i = up[i]; return i; };
+      u32 nclass = nq, nopen = nq;
+      while (nopen > 1 && nclass > 1) {
+        for (u32 i = 0; i < nq; i++) {                   // one expansion per growing search
+          const u32 x = cur[i];
+          if (x == NONE) continue;
+          cur[i] = x == last[i] ? NONE : g.m.w(VN + x);
+          g.for_each_nbr(x, g.arec(x), [&](u32 y) {
+            if (!is_evicted(g.state(y))) return;
+            const u32 sy = g.m.w(g.L.stamp + y);
+            if ((sy & ~31u) == ep) {                     // met another search: same piece
+              const u32 a = root(i), b = root(sy & 31u);
+              if (a != b) { up[b] = a; nclass--; }
+              return;
+            }
+            const uint4 ry = g.srec(y);
+            g.m.w(g.L.stamp + y) = ep | i;
+            g.m.w(VN + y) = NONE;
+            g.m.w(VN + last[i]) = y;
+            last[i] = y;
+            if (cur[i] == NONE) cur[i] = y;
+            cst[i] += ry.y; sz[i]++; nmc[i] += ry.z == cc.z ? 1u : 0u;
+          });
+        }
+        // growing groups: a group is growing while any of its searches has a queue
+        u32 open = 0;
+        for (u32 i = 0; i < nq; i++) if (up[i] == i) {
+          bool g2 = false;
+          for (u32 j = 0; j < nq && !g2; j++) if (cur[j] != NONE && root(j) == i) g2 = true;
+          open += g2;
+        }
+        nopen = open;
+      }
+      if (nclass > 1) {
+        // the group that keeps label c: the growing one, else the largest
+        u32 keep = NONE, best = 0;
+        for (u32 i = 0; i < nq; i++) if (cur[i] != NONE) keep = root(i);
+        if (keep == NONE) {
+          for (u32 i = 0; i < nq; i++) if (up[i] == i) {
+            u32 tot = 0;
+            for (u32 j = 0; j < nq; j++) if (root(j) == i) tot += sz[j];
+            if (tot > best) { best = tot; keep = i; }
+          }
+        }
+        for (u32 r = 0; r < nq; r++) {                   // every other group is a whole piece
+          if (up[r] != r || r == keep) continue;
+          const u32 nc = comp_alloc();
+          u32 pc = 0, ps = 0, pm = 0, plst = NONE;
+          for (u32 j = 0; j < nq; j++) {
+            if (root(j) != r) continue;
+            pc += cst[j]; ps += sz[j];
+            for (u32 x = first[j];; x = g.m.w(VN + x)) {
+              list_unlink(c, x);
+              g.state(x) = O_BIT | nc;
+              g.m.w(g.L.mem_next + x) = plst;
+              g.m.w(g.L.mem_prev + x) = NONE;
+              if (plst != NONE) g.m.w(g.L.mem_prev + plst) = x;
+              plst = x;
+              const u32 l = g.la(x);
+              if (l > pm) pm = l;
+              if (x == last[j]) break;
+            }
+          }
+          u32 pn = 0;
+          for (u32 x = plst; x != NONE; x = g.m.w(g.L.mem_next + x)) pn += g.la(x) == pm;
+          g.m.w(g.L.comp_head + nc) = plst;
+          g.comp(nc) = make_uint4(pc, pn, pm, ps);
+          for (u32 j = 0; j < nq; j++) if (root(j) == r) nmax -= nmc[j];
+          cost -= pc; size -= ps;
+        }
+      }
     }
+    u32 mx = cc.z;
+    if (nmax == 0) { const uint2 r = comp_rescan_maxla(c); mx = r.x; nmax = r.y; }
+    g.comp(c) = make_uint4(cost, nmax, mx, size);
+  }
+
+  // fallback for k > KS searches: relabel every piece of c \ {t} by BFS from
+  // t's evicted neighbours (c's label is released; t is already unlinked)
+  __device__ void split_all(u32 t, const uint4 &ar, u32 c) {
     comp_release(c);
-    u32 ep = ++s.epoch;
+    const u32 ep = next_epoch();
     g.for_each_nbr(t, ar, [&](u32 q) {
       u32 sq = g.state(q);
-      if (!is_evicted(sq) || g.m.w(g.L.stamp + q) == ep) return;
+      if (!is_evicted(sq) || (g.m.w(g.L.stamp + q) & ~31u) == ep) return;
       const u32 nc = comp_alloc();
       u32 head = 0, tail = 0;
       g.m.w(g.L.bfs_q + tail++) = q;
       g.m.w(g.L.stamp + q) = ep;
-      u64 cost = 0;
-      u32 mx = 0, list = NONE, size = 0;
+      u32 cost = 0, mx = 0, nm = 0, list = NONE, size = 0;
       while (head < tail) {
         u32 x = g.m.w(g.L.bfs_q + head++);
         const uint4 sx = g.srec(x);
@@ -262,24 +374,26 @@ struct Leader {
         list = x;
         size++;
         cost += sx.y;
-        mx = sx.z > mx ? sx.z : mx;
+        if (sx.z > mx) { mx = sx.z; nm = 1; } else if (sx.z == mx) nm++;
         g.for_each_nbr(x, ax, [&](u32 y) {
-          if (is_evicted(g.state(y)) && g.m.w(g.L.stamp + y) != ep) {
+          if (is_evicted(g.state(y)) && (g.m.w(g.L.stamp + y) & ~31u) != ep) {
             g.m.w(g.L.stamp + y) = ep;
             g.m.w(g.L.bfs_q + tail++) = y;
           }
         });
       }
       g.m.w(g.L.comp_head + nc) = list;
-      g.comp(nc) = make_uint4((u32)cost, (u32)(cost >> 32), mx, size);
+      g.comp(nc) = make_uint4(cost, nm, mx, size);
     });
   }
 
-  // V2 release of an evicted tensor: its la dropped to -inf; rescan the max if it was the max.
+  // V2 release of an evicted tensor: its la dropped from `old` to -inf (0)
   __device__ __forceinline__ void lower_maxla_exact(u32 t, u32 old) {
-    u32 c = g.state(t) & COMP_MASK;
-    if (old != g.comp(c).z) return;
-    g.comp(c).z = comp_rescan_maxla(c);
+    const u32 c = g.state(t) & COMP_MASK;
+    uint4 cc = g.comp(c);
+    if (old != cc.z || old == 0) return;
+    if (--cc.y == 0) { const uint2 r = comp_rescan_maxla(c); cc.z = r.x; cc.y = r.y; }
+    g.comp(c) = cc;
   }
 
   // ------------------------------------------------------------- union-find
@@ -366,10 +480,16 @@ struct Leader {
     g.m.w(g.L.node_of + t) = NONE;
   }
 
-  __device__ __forceinline__ void raise_maxla(u32 p, u32 sp, u32 v) {
+  // la(p) of an evicted p rose from old to v (make_tensor of a child)
+  __device__ __forceinline__ void raise_maxla(u32 p, u32 sp, u32 old, u32 v) {
     if (s.heuristic == H_DTR) {
-      u32 c = sp & COMP_MASK;
-      if (v > g.comp(c).z) g.comp(c).z = v;
+      if (v == old) return;
+      const u32 c = sp & COMP_MASK;
+      uint4 cc = g.comp(c);
+      if (v > cc.z) { cc.z = v; cc.y = 1; }
+      else if (v == cc.z) cc.y++;
+      else return;                        // v < max: old < v < max, the holders are unchanged
+      g.comp(c) = cc;
     } else if (uses_uf(s.heuristic)) {
       u32 r = uf_find(g.m.w(g.L.node_of + p));
       if (v > g.uf(r).z) g.uf(r).z = v;
@@ -547,10 +667,11 @@ struct Leader {
         if (g.L.linked) g.crec(id) = make_uint2(NONE, 0);
         for (u32 j = 0; j < pr.y; j++) {          // p.C u= {t}; p.last_accessed := clock
           u32 p = g.par(pr.x + j);
+          const u32 old = g.la(p);
           g.la(p) = now;
           pool_rekey(p);
           u32 sp = g.state(p);
-          if (is_evicted(sp)) raise_maxla(p, sp, now);
+          if (is_evicted(sp)) raise_maxla(p, sp, old, now);
         }
         s.n_alloc++;
         root = id; post = 1;

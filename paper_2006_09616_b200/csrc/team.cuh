@@ -63,7 +63,7 @@ __device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const ui
     nd++;
     c3 = c2; c2 = c1; c1 = c0; c0 = c;
     uint4 cr = UF ? g.uf(c) : g.comp(c);
-    sum += mk64(cr.x, cr.y);
+    sum += UF ? mk64(cr.x, cr.y) : (u64)cr.x;   // exact comp record {cost, nmax, maxla, size}
     L = cr.z > L ? cr.z : L;
   });
   bytes += 8ull * nb + 12ull * nd + extra;
@@ -341,7 +341,7 @@ __device__ __forceinline__ void nbr_components_phased(const Sim<SM> &g, const ui
   for (u32 j = 0; j < NB; j++) {            // distinct component records, all in flight
     if (ch[j] != NONE) {
       const uint4 r = UF ? g.uf(ch[j]) : g.comp(ch[j]);
-      cc[j] = r.x; cl[j] = r.z; ch[j] = r.y;   // ch reused: cost high word
+      cc[j] = r.x; cl[j] = r.z; ch[j] = UF ? r.y : 0u;   // ch reused: cost high word (exact comps: u32 cost)
       nd++;
     } else {
       cc[j] = 0; cl[j] = 0; ch[j] = 0;
@@ -464,7 +464,7 @@ __device__ __forceinline__ void nbr_components_warp(const Sim<false> &g, u32 t, 
     }
     if (first) {
       const uint4 r = UF ? g.uf(lab) : g.comp(lab);
-      s += mk64(r.x, r.y);
+      s += UF ? mk64(r.x, r.y) : (u64)r.x;
       mx = r.z > mx ? r.z : mx;
       bytes += 12;
     }

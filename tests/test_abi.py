@@ -46,7 +46,7 @@ def test_workspace_sizes():
 
 def test_cell_and_row_layout():
     import paper_2006_09616_b200 as P
-    assert P.CELL_DTYPE.itemsize == 64 and P.RESULT_DTYPE.itemsize == 88 and P.TRACE_DTYPE.itemsize == 32
+    assert P.CELL_DTYPE.itemsize == 64 and P.RESULT_DTYPE.itemsize == 96 and P.TRACE_DTYPE.itemsize == 32
 
 
 def test_product_path_does_not_import_oracle():
