@@ -82,8 +82,9 @@ static void vremove(vec32 *a, uint32_t x) {
 }
 
 /* One union-find node: parent pointer, running cost sum, and the
- * max last_access of the set (reading C-9). */
-typedef struct { uint64_t parent; uint64_t cost; int64_t maxla; } uf_node;
+ * max last_access of the set (reading C-9); size = nodes in the tree below it
+ * (union by size keeps find O(log n); it shapes the tree, not the sets). */
+typedef struct { uint64_t parent; uint64_t cost; int64_t maxla; uint64_t size; } uf_node;
 
 typedef struct {
   /* configuration */
@@ -178,7 +179,7 @@ static uint64_t uf_new_empty(Sim *s) {
     s->uf = (uf_node *)realloc(s->uf, s->uf_cap * sizeof(uf_node));
   }
   uint64_t x = s->uf_n++;
-  s->uf[x].parent = x; s->uf[x].cost = 0; s->uf[x].maxla = NEG_INF;
+  s->uf[x].parent = x; s->uf[x].cost = 0; s->uf[x].maxla = NEG_INF; s->uf[x].size = 1;
   return x;
 }
 
@@ -191,7 +192,9 @@ static uint64_t uf_find(Sim *s, uint64_t x) {
 static void uf_union(Sim *s, uint64_t a, uint64_t b) {
   a = uf_find(s, a); b = uf_find(s, b);
   if (a == b) return;
+  if (s->uf[a].size < s->uf[b].size) { uint64_t x = a; a = b; b = x; }   /* union by size */
   s->uf[b].parent = a;
+  s->uf[a].size += s->uf[b].size;
   s->uf[a].cost += s->uf[b].cost;
   if (s->uf[b].maxla > s->uf[a].maxla) s->uf[a].maxla = s->uf[b].maxla;   /* reading C-9 */
 }
