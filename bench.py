@@ -435,7 +435,7 @@ def config5(P, torch, dev, cap=2000, rank=0, ws=1):
         local = rs.rows_device()
         if local is None:
             local = torch.zeros(0, dtype=torch.uint8, device=dev)
-        return sweep.gather_rows(local, len(shards[rank]), max_local, ws)   # numpy rows of every rank
+        return sweep.gather_rows(local, [len(x) for x in shards], ws)   # numpy rows of every rank
 
     once()
     torch.cuda.synchronize()

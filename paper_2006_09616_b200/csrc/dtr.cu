@@ -41,7 +41,7 @@ int dtr_version(void) { return 1; }
 
 #ifdef DTR_PROFILE
 int dtr_debug_profile(unsigned long long *out, int reset) {
-  for (int i = 0; i < 16; i++) out[i] = 0;
+  for (int i = 0; i < 32; i++) out[i] = 0;
   CK(prof_read_cta_cl(out, reset));
   CK(prof_read_cta_nocl(out, reset));
   CK(prof_read_grid(out, reset));
@@ -165,7 +165,7 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
     while (i < n_cells) {
       u64 need;
       const int c = cls_of(i, &need);
-      u64 smem = c == 2 ? 0 : need;
+      u64 smem = c == 2 ? CTA_WQ_BYTES : need;   // global state: only the per-warp slow stacks
       u32 j = i + 1;
       bool cl = uses_closure(h_dims[3 * i + 2]);
       for (; j < n_cells; j++) {

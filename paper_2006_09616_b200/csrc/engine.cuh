@@ -43,7 +43,8 @@
 // [0] leader resume cycles, [1] warp-team score cycles, [2] warp reduce cycles,
 // [3] warp-team decisions, [4] cta-team cycles, [5] cta-team decisions, [6] init cycles,
 // [8/9] record_and_evict cycles/calls, [10/11] complete_top, [12/13] push, [14] resume loop iterations
-static __device__ unsigned long long g_prof[16];
+#define PROF_N 32
+static __device__ unsigned long long g_prof[PROF_N];
 #define PROF_T(x) unsigned long long x = clock64()
 #define PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
 #else
@@ -85,6 +86,12 @@ __host__ __device__ __forceinline__ bool int_key_heur(u32 h) { return h == H_SIZ
 __host__ __device__ __forceinline__ bool uses_uf(u32 h) { return h == H_DTR_EQ || (is_abl(h) && abl_c(h) == ABL_EQCLASS); }
 enum { OP_MAKE = 1, OP_GET = 2, OP_RELEASE = 3, OP_REMAT = 4, OP_ENSURE = 5, OP_DEBUG_EVICT = 6,
        OP_SCORES = 7 /* per-call only: score the whole pool */ };
+// Cached closure sums (App. C "Caching metadata"): the
+// leader queues every tensor whose evicted status flips (evict, finished
+// rematerialization, V1 banish of an evicted tensor); before the next score
+// pass the team walks from each queued tensor and marks stale the caches it may
+// have changed.  More than EVQ_CAP events between two decisions = all stale.
+constexpr u32 EVQ_CAP = 64;
 enum { DEALLOC_V2 = 0, DEALLOC_V1 = 1, DEALLOC_EAGER = 2, DEALLOC_IGNORE = 3 };
 enum { ST_OK = 0, ST_INVAL = 1, ST_PRECOND = 2, ST_OOM = 3, ST_THRASH = 4, ST_CAPACITY = 5,
        ST_STATE = 6, ST_DECISION_CAP = 8 };
@@ -106,7 +113,8 @@ struct Lay {
   u32 msps_bm, msps_q, msps_words, msps_warps;         // closure BFS scratch: msps_warps slots
   u32 msps_lock;                                       // grid: slot locks (0 = CTA: slot = warp)
   u32 e_next, e_child;                                 // linked children (per-call)
-  u32 slowq;                                           // whole-GPU team: candidates with nev > 0
+  u32 ccache, evq;                                     // closure cache {up+1, down+1} per tensor (0 = stale)
+                                                       // + the leader's event queue (batch engines only)
   u32 words;                                           // total
 };
 
@@ -140,6 +148,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
   L.node_of = L.uf = L.uf_size = L.uf_cap = 0;
   L.msps_bm = L.msps_q = L.msps_words = L.msps_warps = L.msps_lock = 0;
   L.e_next = L.e_child = 0;
+  L.ccache = L.evq = 0;
   if (heur == H_DTR) {
     L.mem_next = take(n1);
     L.mem_prev = take(n1);
@@ -159,12 +168,15 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
     L.msps_bm = take((u64)L.msps_words * msps_warps);
     L.msps_q = take(n1 * msps_warps);
     if (grid) L.msps_lock = take(msps_warps);
+    if (!linked) {                                     // cached closure sums
+      L.ccache = take(2 * n1);
+      L.evq = take(EVQ_CAP);
+    }
   }
   if (linked) {
     L.e_next = take(e1);
     L.e_child = take(e1);
   }
-  L.slowq = grid ? take(n1) : 0;
   L.words = (u32)o;
   return o < 0xFFFFFFF0ull;
 }
@@ -225,6 +237,7 @@ struct Scalars {
   u32 dealloc;        // DEALLOC_*: what release does at rho = 0 (reading C-22)
   u32 comp_top;       // h_DTR: free label slots on the stack
   u32 comp_fresh;     // h_DTR: label slots never used yet
+  u32 ev_n;           // closure cache: events queued since the last score pass (EVQ_CAP + 1 = overflow)
   u64 kill_limit;     // min(thrash_kill * base_so_far, CLOCK_LIMIT) (recomputed at every MAKE; kill 0 = off)
 };
 
@@ -315,6 +328,7 @@ struct Sim {
   __device__ __forceinline__ u32 &pool_pos(u32 t) const { return m.w(L.pool_pos + t); }
   __device__ __forceinline__ uint4 &comp(u32 c) const { return m.q(L.comp + 4 * c); }
   __device__ __forceinline__ uint4 &uf(u32 x) const { return m.q(L.uf + 4 * x); }
+  __device__ __forceinline__ uint2 &ccache(u32 t) const { return m.d(L.ccache + 2 * t); }   // {up+1, down+1}
 
   // parents of t then children (ar = arec(t) already loaded; linked lists are
   // re-read from the live head)

@@ -218,11 +218,11 @@ cudaError_t launch_adv(u32 n_runs, u32 smem, cudaStream_t st, const dtr_adversar
 
 #ifdef DTR_PROFILE
 cudaError_t prof_read_adv(unsigned long long *out, int reset) {
-  unsigned long long v[16];
+  unsigned long long v[PROF_N];
   cudaError_t e = cudaMemcpyFromSymbol(v, g_prof, sizeof v);
   if (e != cudaSuccess) return e;
-  for (int i = 0; i < 16; i++) out[i] += v[i];
-  if (reset) { unsigned long long z[16] = {0}; e = cudaMemcpyToSymbol(g_prof, z, sizeof z); }
+  for (int i = 0; i < PROF_N; i++) out[i] += v[i];
+  if (reset) { unsigned long long z[PROF_N] = {0}; e = cudaMemcpyToSymbol(g_prof, z, sizeof z); }
   return e;
 }
 #endif

@@ -29,6 +29,7 @@ __device__ __forceinline__ Cmd shfl_cmd(const Cmd &c) {
   r.seed = __shfl_sync(0xffffffffu, c.seed, 0);
   r.heur = __shfl_sync(0xffffffffu, c.heur, 0);
   r.n_ids = __shfl_sync(0xffffffffu, c.n_ids, 0);
+  r.n_ev = __shfl_sync(0xffffffffu, c.n_ev, 0);
   return r;
 }
 
@@ -48,6 +49,8 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   PROF_T(ti1);
   if (tid == 0) PROF_ADD(6, ti1 - ti0);
   u64 bytes = 0, evals = 0;
+  // global-memory state: the dynamic shared memory holds the per-warp slow stacks (score_stream)
+  u32 *wq = SM ? nullptr : g_smem + warp * SLOWQ;
   if (warp == 0) {
     Leader<SM, false> L;
     if (lane == 0) leader_init(L, g, logw, cell, trace);
@@ -64,6 +67,9 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
         PROF_ADD(0, t1 - t0);
       }
       c = shfl_cmd(c);
+      if constexpr (CL) {   // closure caches: warp 0 walks the queued events (slot 0) before any scoring
+        if (c.kind == CMD_ARGMIN && c.n_ev) closure_events(g, c, 0, sh.msps_tail);
+      }
       if (c.kind == CMD_ARGMIN && c.pool_size <= WARP_TEAM_MAX && g.L.pool_key) {   // size / LRU: 64-bit keys
         PROF_T(t2);
         const u64 k = warp_min64(team_intkey_min(g, c, lane, 32, bytes, evals));
@@ -74,7 +80,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       if (c.kind == CMD_ARGMIN && c.pool_size <= WARP_TEAM_MAX) {
         PROF_T(t2);
         u32 bk;
-        Cand best = team_score<SM, false, false, CL>(g, c, lane, 32, 0, 1, sh.msps_tail, bytes, evals, bk);
+        Cand best = team_score<SM, false, false, CL>(g, c, lane, 32, 0, 1, sh.msps_tail, bytes, evals, bk, wq);
         PROF_T(t3);
         best = warp_argmin_fast(best, bk, int_key_heur(c.heur));
         PROF_T(t4);
@@ -86,7 +92,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       __syncthreads();
       if (c.kind != CMD_ARGMIN) break;
       u32 bk;
-      Cand best = team_score<SM, false, false, CL>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk);
+      Cand best = team_score<SM, false, false, CL>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk, wq);
       best = block_argmin(best, bk, sh.red, int_key_heur(c.heur));
       PROF_T(t6);
       if (lane == 0) { res = best; have = true; PROF_ADD(4, t6 - t5); PROF_ADD(5, 1); }
@@ -98,7 +104,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       const Cmd c = sh.cmd;
       if (c.kind != CMD_ARGMIN) break;
       u32 bk;
-      Cand best = team_score<SM, false, false, CL>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk);
+      Cand best = team_score<SM, false, false, CL>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk, wq);
       block_argmin(best, bk, sh.red, int_key_heur(c.heur));
     }
   }

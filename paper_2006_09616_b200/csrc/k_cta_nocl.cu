@@ -14,11 +14,11 @@ cudaError_t launch_cta_nocl(u32 n_blocks, u32 smem, cudaStream_t st, const u32 *
 
 #ifdef DTR_PROFILE
 cudaError_t prof_read_cta_nocl(unsigned long long *out, int reset) {
-  unsigned long long v[16];
+  unsigned long long v[PROF_N];
   cudaError_t e = cudaMemcpyFromSymbol(v, g_prof, sizeof v);
   if (e != cudaSuccess) return e;
-  for (int i = 0; i < 16; i++) out[i] += v[i];
-  if (reset) { unsigned long long z[16] = {0}; e = cudaMemcpyToSymbol(g_prof, z, sizeof z); }
+  for (int i = 0; i < PROF_N; i++) out[i] += v[i];
+  if (reset) { unsigned long long z[PROF_N] = {0}; e = cudaMemcpyToSymbol(g_prof, z, sizeof z); }
   return e;
 }
 #endif

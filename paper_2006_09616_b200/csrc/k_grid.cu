@@ -12,6 +12,7 @@ struct __align__(16) GridShared {
   RedSmem red;
   ScanSmem scan;
   u32 msps_tail[GRID_THREADS / 32];
+  u32 wq[GRID_THREADS / 32][SLOWQ];   // per-warp stacks of deferred (slow) candidates
 };
 
 struct GridSync {
@@ -44,8 +45,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
   cell_layout(g.L, logw[2], logw[3], cell.heuristic, DTR_ENGINE_GRID);
   const u32 rank = blockIdx.x * blockDim.x + tid, size = gridDim.x * blockDim.x;
   const u32 wrank = rank >> 5, wsize = size >> 5;
-  u32 *slown = (u32 *)(ws + WS_SLOWN);
-  if (rank == 0) { gstats[0] = 0; gstats[1] = 0; *slown = 0; }
+  if (rank == 0) { gstats[0] = 0; gstats[1] = 0; *(u32 *)(ws + WS_PA_DONE) = 0; }
   init_sim(g, logw, rank, size, blockIdx.x == 0, sh.scan, GridSync());
   Leader<false, true> L;
   if (rank == 0) leader_init(L, g, logw, cell, trace);
@@ -54,16 +54,28 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
   u64 bytes = 0, evals = 0;
   PROF_T(tg0);
   for (;;) {
-    if (rank == 0) {
-      PROF_T(a0);
-      const u32 kind = L.resume(have, res);
-      have = false;
+    if (rank < 32) {                // the leader's warp
       Cmd c;
-      publish(c, kind, L.s);
-      *gcmd = c;
-      *slown = 0;                   // every warp has finished reading it (grid barrier since)
-      PROF_T(a1);
-      PROF_ADD(0, a1 - a0);
+      u32 n_ev = 0, kind = 0;
+      if (rank == 0) {
+        PROF_T(a0);
+        kind = L.resume(have, res);
+        have = false;
+        publish(c, kind, L.s);
+        n_ev = c.n_ev;
+        PROF_T(a1);
+        PROF_ADD(0, a1 - a0);
+      }
+      // closure caches: the warp walks the queued events (slot 0; every other
+      // warp is parked at the barrier below) before any scoring
+      n_ev = __shfl_sync(0xffffffffu, n_ev, 0);
+      kind = __shfl_sync(0xffffffffu, kind, 0);
+      if (kind == CMD_ARGMIN && n_ev) {
+        Cmd e;
+        e.n_ev = n_ev; e.kind = kind; e.heur = cell.heuristic; e.n_ids = __shfl_sync(0xffffffffu, L.s.n_alloc, 0);
+        closure_events(g, e, 0, sh.msps_tail);
+      }
+      if (rank == 0) *gcmd = c;
     }
     PROF_T(b0);
     grid.sync();
@@ -74,6 +86,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
       c.kind = __ldcg(&gcmd->kind); c.pool_size = __ldcg(&gcmd->pool_size); c.clock = __ldcg(&gcmd->clock);
       c.decisions = __ldcg(&gcmd->decisions); c.seed = __ldcg(&gcmd->seed); c.heur = __ldcg(&gcmd->heur);
       c.n_ids = __ldcg(&gcmd->n_ids);
+      c.n_ev = __ldcg(&gcmd->n_ev);
       sh.cmd = c;
     }
     __syncthreads();
@@ -81,7 +94,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
     u32 bk;
     PROF_T(c0);
     Cand best = team_score<false, true, true>(g, sh.cmd, rank, size, wrank, wsize, sh.msps_tail, bytes, evals, bk,
-                                              slown);
+                                              sh.wq[tid >> 5]);
     PROF_T(c1);
     const bool ik = int_key_heur(sh.cmd.heur);
     best = block_argmin(best, bk, sh.red, ik);
@@ -115,12 +128,16 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
 
 // ---------------------------------------------------------------------------
 // K3+K4 alone: score the current pool of the simulation left in a grid-engine
-// workspace and reduce its argmin (last-block reduction, no cooperative sync).
-// Used to time the score pass in isolation (bench roofline_large_pool).
+// workspace and reduce its argmin.  A plain (non-cooperative) persistent launch:
+// every block writes its partial, and the LAST block to finish (a counter in
+// the workspace header) reduces them -- no grid barrier anywhere.  Used to time
+// the score pass in isolation (bench roofline_large_pool).
 // ---------------------------------------------------------------------------
 struct __align__(16) PaShared {
   RedSmem red;
   u32 msps_tail[PA_THREADS / 32];
+  u32 wq[PA_THREADS / 32][SLOWQ];
+  u32 last;
 };
 
 __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *logw, u32 heur, char *ws,
@@ -128,7 +145,7 @@ __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *l
   __shared__ PaShared sh;
   const u32 tid = threadIdx.x;
   Cand *partials = (Cand *)(ws + WS_PARTIALS);
-  u32 *slown = (u32 *)(ws + WS_SLOWN);
+  u32 *done = (u32 *)(ws + WS_PA_DONE);          // blocks finished (the last one resets it)
   Sim<false> g;
   g.m.gbase = (u32 *)(ws + WS_HEADER);
   cell_layout(g.L, logw[2], logw[3], heur, DTR_ENGINE_GRID);
@@ -136,11 +153,12 @@ __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *l
   Cmd cmd;
   cmd.kind = CMD_ARGMIN; cmd.pool_size = sc->pool_size; cmd.clock = sc->clock; cmd.decisions = sc->decisions;
   cmd.seed = sc->seed; cmd.heur = heur; cmd.n_ids = sc->n_alloc;
+  cmd.n_ev = NONE;                 // the closure caches may lag the last decisions' events
   const u32 rank = blockIdx.x * blockDim.x + tid, size = gridDim.x * blockDim.x;
   u64 bytes = 0, evals = 0;
   u32 bk;
   Cand best = team_score<false, true, true>(g, cmd, rank, size, rank >> 5, size >> 5, sh.msps_tail, bytes, evals, bk,
-                                            slown);
+                                            sh.wq[tid >> 5]);
   const bool ik = int_key_heur(heur);
   best = block_argmin(best, bk, sh.red, ik);
   block_sum2(bytes, evals, sh.red);
@@ -149,9 +167,12 @@ __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *l
     partials[blockIdx.x] = best;
     bstats[2 * blockIdx.x] = bytes;
     bstats[2 * blockIdx.x + 1] = evals;
+    __threadfence();
+    sh.last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
-  cg::this_grid().sync();
-  if (blockIdx.x == 0) {      // block 0 reduces the partials (all loads in flight)
+  __syncthreads();
+  if (sh.last) {                 // the last block reduces the partials (all loads in flight)
+    __threadfence();
     Cand c = cand_none();
     u32 ck = KEY_NONE;
     u64 tb = 0, te = 0;
@@ -165,7 +186,7 @@ __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *l
     c = block_argmin(c, ck, sh.red, ik);
     Cand w = c;
     block_sum2(tb, te, sh.red);
-    if (tid == 0) { out[0] = w.num; out[1] = w.den; out[2] = w.id; out[3] = tb; out[4] = te; *slown = 0; }
+    if (tid == 0) { out[0] = w.num; out[1] = w.den; out[2] = w.id; out[3] = tb; out[4] = te; *done = 0; }
   }
 }
 
@@ -189,17 +210,17 @@ cudaError_t launch_grid(int blocks, cudaStream_t st, const u32 *words, const dtr
 }
 
 cudaError_t launch_pool_argmin(int blocks, cudaStream_t st, const u32 *logw, u32 heur, char *ws, u64 *out) {
-  void *args[] = {(void *)&logw, (void *)&heur, (void *)&ws, (void *)&out};
-  return cudaLaunchCooperativeKernel((void *)pool_argmin_kernel, dim3(blocks), dim3(PA_THREADS), args, 0, st);
+  pool_argmin_kernel<<<blocks, PA_THREADS, 0, st>>>(logw, heur, ws, out);
+  return cudaGetLastError();
 }
 
 #ifdef DTR_PROFILE
 cudaError_t prof_read_grid(unsigned long long *out, int reset) {
-  unsigned long long v[16];
+  unsigned long long v[PROF_N];
   cudaError_t e = cudaMemcpyFromSymbol(v, g_prof, sizeof v);
   if (e != cudaSuccess) return e;
-  for (int i = 0; i < 16; i++) out[i] += v[i];
-  if (reset) { unsigned long long z[16] = {0}; e = cudaMemcpyToSymbol(g_prof, z, sizeof z); }
+  for (int i = 0; i < PROF_N; i++) out[i] += v[i];
+  if (reset) { unsigned long long z[PROF_N] = {0}; e = cudaMemcpyToSymbol(g_prof, z, sizeof z); }
   return e;
 }
 #endif

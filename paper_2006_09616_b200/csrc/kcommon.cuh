@@ -39,8 +39,9 @@ using namespace dtr;
 #define WS_BSTATS 98816      /* per-block {bytes, evals} for dtr_pool_argmin */
 #define WS_SCALARS 128       /* grid engine: final Scalars of the last cell */
 #define WS_PARTIALS 512
-#define WS_SLOWN 124         /* whole-GPU team: slow-queue length (u32) */
-#define CTA_SMEM_MAX (225u * 1024u)  /* + ~1 KB static CtaShared <= 227 KB per block */
+#define WS_PA_DONE 124       /* dtr_pool_argmin: blocks finished (u32; zeroed by the grid engine) */
+#define CTA_SMEM_MAX (225u * 1024u)
+#define CTA_WQ_BYTES (CTA_THREADS / 32 * SLOWQ * 4)   /* global-state cells: per-warp slow stacks (team.cuh) */  /* + ~1 KB static CtaShared <= 227 KB per block */
 
 // ---------------------------------------------------------------------------
 // Initialisation (team-parallel): static records and parents from the log,
@@ -97,6 +98,7 @@ __device__ void init_sim(const Sim<SM> &g, const u32 *logw, u32 rank, u32 size, 
     g.m.w(g.L.fr + t) = 0;                      // fill cursor (the stack is unused until the leader starts)
     if (heur == H_DTR) g.m.w(g.L.stamp + t) = 0;
     if (uses_uf(heur)) g.m.w(g.L.node_of + t) = NONE;
+    if (g.L.ccache) g.ccache(t) = make_uint2(0, 0);
   }
   for (u32 j = rank; j < E; j += size) g.par(j) = lpar[j];
   for (u32 w = rank; w < g.L.pool_words; w += size) g.pool_word(w) = 0;
@@ -178,9 +180,13 @@ static __device__ void write_row(dtr_result &r, const Scalars &s, u64 bytes, u64
   r = x;
 }
 
-__device__ __forceinline__ void publish(Cmd &c, u32 kind, const Scalars &s) {
+// the closure-cache events travel with an ARGMIN command (the team processes
+// them before scoring) and are consumed by it
+__device__ __forceinline__ void publish(Cmd &c, u32 kind, Scalars &s) {
   c.kind = kind; c.pool_size = s.pool_size; c.clock = s.clock; c.decisions = s.decisions;
   c.seed = s.seed; c.heur = s.heuristic; c.n_ids = s.n_alloc;
+  c.n_ev = s.ev_n;
+  if (kind == CMD_ARGMIN) s.ev_n = 0;
 }
 
 template <bool SM, bool BM>

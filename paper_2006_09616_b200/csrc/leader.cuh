@@ -28,6 +28,7 @@ enum { CMD_DONE = 0, CMD_ARGMIN = 1, CMD_SCORES = 2 };
 struct Cmd {
   u64 clock, decisions, seed;
   u32 kind, pool_size, heur, n_ids;   // n_ids: tensor ids [0, n_ids) to scan for pool members
+  u32 n_ev;                           // closure cache: events queued (NONE: do not use the cache)
 };
 
 template <bool SM, bool BM>
@@ -138,6 +139,7 @@ struct Leader {
       s.M -= sr.x;
       pool_remove(t);
     } else if (is_evicted(st)) {                     // leaves its evicted component
+      ev_push(t);
       nev_add(t, ar, NONE);
       if (s.heuristic == H_DTR) remat_exact(t, ar, st & COMP_MASK);
       else if (uses_uf(s.heuristic)) remat_uf(t, sr.y);
@@ -496,10 +498,20 @@ struct Leader {
     }
   }
 
+  // ------------------------------------------------------------- closure-cache events
+  // t's evicted status flipped: queue it for the team's invalidation walk
+  __device__ __forceinline__ void ev_push(u32 t) {
+    if (!g.L.ccache) return;
+    const u32 k = s.ev_n;
+    if (k < EVQ_CAP) g.m.w(g.L.evq + k) = t;
+    if (k <= EVQ_CAP) s.ev_n = k + 1;
+  }
+
   // ------------------------------------------------------------- evict
   __device__ __forceinline__ void evict(u32 t) {
     const uint4 sr = g.srec(t);
     const uint4 ar = g.arec(t);
+    ev_push(t);
     g.state(t) = O_BIT;
     s.M -= sr.x;
     pool_remove(t);
@@ -560,6 +572,7 @@ struct Leader {
     s.computations++;
     if (st & O_BIT) {
       s.remats++;
+      ev_push(t);
       nev_add(t, ar, NONE);
       if (s.heuristic == H_DTR) remat_exact(t, ar, st & COMP_MASK);
       else if (uses_uf(s.heuristic)) remat_uf(t, sr.y);

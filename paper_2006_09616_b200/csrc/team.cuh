@@ -77,7 +77,7 @@ __device__ __forceinline__ void nbr_components(const Sim<SM> &g, u32 t, const ui
 // c0 is returned in every lane.
 template <bool SM>
 __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &ar, u32 wslot, volatile u32 *tail, u64 &bytes,
-                            u32 t = NONE, bool down = false) {
+                            u32 t = NONE, bool down = false, u64 *up_out = nullptr) {
   const u32 lane = threadIdx.x & 31;
   const u32 bm = g.L.msps_bm + wslot * g.L.msps_words;
   const u32 q = g.L.msps_q + wslot * (g.L.n + 1);
@@ -110,6 +110,7 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &ar, u32 wslot, volati
     tl = *tail;
     __syncwarp();
   }
+  u64 up = sum;
   if (down) {                                   // evicted descendants through evicted children
     auto children = [&](u32 x) {
       const uint2 cr = g.crec(x);
@@ -132,8 +133,86 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &ar, u32 wslot, volati
   for (u32 i = lane; i < tl; i += 32) g.m.w(bm + (g.m.w(q + i) >> 5)) = 0;
   __syncwarp();
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    up += __shfl_xor_sync(0xffffffffu, up, o);
+  }
+  if (up_out) *up_out = up;
   return sum;
+}
+
+// Closure-cache invalidation (App. C "Caching metadata"), run by
+// ONE warp before a score pass over the events the leader queued since the
+// last one (tensors whose evicted status flipped).  A flip of x can change
+// e_R(t) only for the non-evicted t reached from x downwards through evicted
+// tensors (the flipped tensor on the changed path closest to t sees only
+// evicted tensors between itself and t, in the current state), and the
+// descendant half of e*(t) only for the non-evicted t reached upwards; those
+// caches (and x's own) are marked stale.  Walks use the current state, so the
+// order of the events does not matter.  Scratch: closure slot `slot`.
+template <bool SM>
+__device__ void closure_events(const Sim<SM> &g, const Cmd &cmd, u32 slot, volatile u32 *tail) {
+  if (!g.L.ccache || cmd.n_ev == 0 || cmd.n_ev == NONE) return;
+  const u32 lane = threadIdx.x & 31;
+  const bool down = cmd.heur != H_MSPS;
+  if (cmd.n_ev > EVQ_CAP) {                      // overflow: every cache is stale
+    for (u32 t = lane; t < cmd.n_ids; t += 32) g.ccache(t) = make_uint2(0, 0);
+    __syncwarp();
+    return;
+  }
+  const u32 bm = g.L.msps_bm + slot * g.L.msps_words;
+  const u32 q = g.L.msps_q + slot * (g.L.n + 1);
+  PROF_T(ce0);
+  for (u32 e = 0; e < cmd.n_ev; e++) {
+    const u32 x = g.m.w(g.L.evq + e);
+    if (lane == 0) { g.ccache(x) = make_uint2(0, 0); *tail = 0; }
+    __syncwarp();
+    // f = 0: ancestor caches (.x) of the tensors below; f = 1: descendant caches (.y) above
+    auto visit = [&](u32 y, u32 f) {
+      if (!is_evicted(g.state(y))) { g.m.w(g.L.ccache + 2 * y + f) = 0; return; }
+      const u32 bit = 1u << (y & 31);
+      if (atomicOr(&g.m.w(bm + (y >> 5)), bit) & bit) return;
+      g.m.w(q + atomicAdd((u32 *)tail, 1u)) = y;
+    };
+    auto kids = [&](u32 y, u32 j0, u32 dj) {
+      const uint2 cr = g.crec(y);
+      for (u32 j = j0; j < cr.y; j += dj) visit(g.m.w(g.L.ch + cr.x + j), 0);
+    };
+    auto pars = [&](u32 y, u32 j0, u32 dj) {
+      const uint2 pr = g.prec(y);
+      for (u32 j = j0; j < pr.y; j += dj) visit(g.par(pr.x + j), 1);
+    };
+    u32 head = 0, tl;
+    kids(x, lane, 32);
+    __syncwarp();
+    tl = *tail;
+    __syncwarp();
+    while (head < tl) {
+      for (u32 i = head + lane; i < tl; i += 32) kids(g.m.w(q + i), 0, 1);
+      __syncwarp();
+      head = tl;
+      tl = *tail;
+      __syncwarp();
+    }
+    if (down) {
+      pars(x, lane, 32);
+      __syncwarp();
+      tl = *tail;
+      __syncwarp();
+      while (head < tl) {
+        for (u32 i = head + lane; i < tl; i += 32) pars(g.m.w(q + i), 0, 1);
+        __syncwarp();
+        head = tl;
+        tl = *tail;
+        __syncwarp();
+      }
+    }
+    for (u32 i = lane; i < tl; i += 32) g.m.w(bm + (g.m.w(q + i) >> 5)) = 0;
+    if (lane == 0) PROF_ADD(20, tl);
+    __syncwarp();
+  }
+  PROF_T(ce1);
+  if (lane == 0) { PROF_ADD(19, cmd.n_ev); PROF_ADD(21, ce1 - ce0); }
 }
 
 // K5 closures of ONE candidate per lane (lane-parallel).  UP: e_R(t), the
@@ -322,11 +401,19 @@ __device__ __forceinline__ void nbr_components_phased(const Sim<SM> &g, const ui
     if constexpr (UF) lab[j] = is_evicted(sq) ? g.m.w(g.L.node_of + q[j]) : NONE;
     else lab[j] = is_evicted(sq) ? (sq & COMP_MASK) : NONE;
   }
-  if constexpr (UF) {
-    u32 steps = 0;
+  if constexpr (UF) {                       // union-find roots: every chain advances one step per round
+    u32 up[NB], steps = 0;
 #pragma unroll
-    for (u32 j = 0; j < NB; j++)
-      if (lab[j] != NONE) { lab[j] = g.uf_root(lab[j], steps); bytes += 4; }
+    for (u32 j = 0; j < NB; j++) { up[j] = lab[j] != NONE ? g.uf(lab[j]).w : NONE; bytes += lab[j] != NONE ? 4 : 0; }
+    for (;;) {
+      bool more = false;
+#pragma unroll
+      for (u32 j = 0; j < NB; j++) more = more || up[j] != lab[j];
+      if (!more) break;
+#pragma unroll
+      for (u32 j = 0; j < NB; j++)
+        if (up[j] != lab[j]) { lab[j] = up[j]; up[j] = g.uf(lab[j]).w; steps++; }
+    }
     bytes += 4ull * steps;
   }
   u32 cc[NB], cl[NB], ch[NB], nd = 0;
@@ -426,8 +513,8 @@ __device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t,
 // shuffle scan against earlier chunks (degree > 32 only).  All lanes return
 // the sum of the distinct adjacent components' cost and the max of their max
 // la with la(t) (sr.z); bytes are counted per lane.
-template <bool UF>
-__device__ __forceinline__ void nbr_components_warp(const Sim<false> &g, u32 t, const uint4 &sr, u64 &sum, u32 &L,
+template <bool SM, bool UF>
+__device__ __forceinline__ void nbr_components_warp(const Sim<SM> &g, u32 t, const uint4 &sr, u64 &sum, u32 &L,
                                                     u64 &bytes) {
   const u32 FULL = 0xffffffffu, lane = threadIdx.x & 31;
   const uint4 ar = g.arec(t);
@@ -500,56 +587,137 @@ __device__ __forceinline__ void score_loop(const Sim<SM> &g, const Cmd &cmd, u32
   }
 }
 
-// Whole-GPU pass over the pool BITMAP (grid engine, dtr_pool_argmin; every
-// thread of a cooperative grid).  Phase 1: warp w takes bitmap words w, w + W,
-// w + 2W, ... (W = warps in the grid) and lane l the id 32 * word + l, so each
-// step reads one broadcast bitmap word and 32 consecutive score records (512 B,
-// coalesced), U steps in flight per lane; a candidate with nev = 0 is scored
-// from its record alone, one with evicted neighbours is appended to the slow
-// queue (one atomic per warp step).  Phase 2 (after a grid barrier): the slow
-// candidates are spread evenly over the grid, one per lane, so no warp
-// serialises a cluster of them; a candidate of degree > NB is resolved by the
-// whole warp (nbr_components_warp).
-template <int H, u32 U>
-__device__ __forceinline__ void score_bm(const Sim<false> &g, const Cmd &cmd, u32 wrank, u32 wsize, Cand &best,
-                                         u32 &bk, u64 &bytes, u64 &evals, u32 *slown) {
+// Key of c/(m (clock + 1 - L)) with no 64-bit arithmetic (nev = 0 candidates
+// of h_DTR / h_DTR_eq): clock < 2^32 - 1 (reading C-14), so s fits u32.  Three
+// u32 -> f32 roundings, one product and __fdividef (<= 2 ulp) give a relative
+// error below 8 * 2^-24, far inside KEY_MARGIN (256 ulps): keys farther apart
+// than the margin order exactly like the rationals.  0 = score 0, KEY_INF = +inf.
+__device__ __forceinline__ u32 stale_key(u32 c, u32 m, u32 L, u32 clock1) {
+  if (L == 0) return 0u;
+  const u32 s = clock1 - L;
+  if (s == 0) return KEY_INF;
+  return __float_as_uint(__fdividef(__uint2float_rn(c), __uint2float_rn(m) * __uint2float_rn(s)));
+}
+
+// Whole-GPU pass over the pool BITMAP (grid engine, dtr_pool_argmin).  Warp w
+// takes bitmap words w, w + W, w + 2W, ... (W = warps in the grid) and lane l
+// the id 32 * word + l, so each step reads one broadcast bitmap word and 32
+// consecutive score records (512 B, coalesced), U steps in flight per lane; a
+// candidate with nev = 0 is scored from its record alone (stale_key: no 64-bit
+// arithmetic unless it is a new best or a near-tie).  A candidate with evicted
+// neighbours is pushed on the warp's shared-memory stack `wq` (SLOWQ entries)
+// and resolved as soon as 32 are waiting -- one per lane, phased gathers
+// (nbr_components_phased); degree > NB: the whole warp (nbr_components_warp) --
+// and the rest after the stream, so no grid barrier separates the two kinds.
+constexpr u32 SLOWQ = 160;   // >= 31 + 4 steps x 32
+
+// BM = false: the same pass over the compact pool list (CTA engine with its
+// state in global memory): lane l of warp w takes pool slots 32 w + l,
+// 32 (w + W) + l, ...; the ids are a coalesced load and the score records a
+// gather, U steps in flight.
+template <bool SM, bool BM, int H, u32 U>
+__device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u32 wrank, u32 wsize, Cand &best,
+                                             u32 &bk, u64 &bytes, u64 &evals, u32 *wq) {
+  static_assert(U * 32 + 31 <= SLOWQ, "slow stack too small");
   const u32 FULL = 0xffffffffu, lane = threadIdx.x & 31;
-  const u32 nwords = (cmd.n_ids + 31) / 32;
+  const u32 nwords = BM ? (cmd.n_ids + 31) / 32 : (cmd.pool_size + 31) / 32;
+  const u32 clock1 = (u32)(cmd.clock + 1);
   constexpr bool NBR = H == H_DTR || H == H_DTR_EQ || H == H_ABL;
+  constexpr bool UF = H != H_DTR;
+  u32 nq = 0;                                  // warp-uniform stack depth
+  // resolve one slow candidate per lane (t = NONE: idle lane)
+  auto resolve = [&](u32 t) {
+    uint4 sr = make_uint4(0, 0, 0, 0), ar = make_uint4(0, 0, 0, 0);
+    if (t != NONE) { sr = g.srec(t); ar = g.arec(t); }
+    const bool big = t != NONE && ar.y + ar.w > NB;
+    auto finish = [&](u32 tt, const uint4 &s4, u64 sum, u32 L) {
+      Cand c;
+      c.id = tt;
+      evals++;
+      bytes += BM ? 16 : 20;                   // score record (+ pool slot)
+      if constexpr (H == H_ABL) abl_finish((u64)s4.y + sum, s4.x, s4.z, cmd, c);
+      else stale_score((u64)s4.y + sum, s4.x, L, cmd.clock, c.num, c.den);
+      cand_take(best, bk, c);
+    };
+    if (t != NONE && !big) {
+      u64 sum;
+      u32 L;
+      nbr_components_phased<SM, UF>(g, sr, ar, sum, L, bytes);
+      finish(t, sr, sum, L);
+    }
+    u32 bm = __ballot_sync(FULL, big);
+    while (bm) {
+      const u32 l = __ffs(bm) - 1;
+      bm &= bm - 1;
+      const u32 tt = __shfl_sync(FULL, t, l);
+      uint4 s4;
+      s4.x = __shfl_sync(FULL, sr.x, l); s4.y = __shfl_sync(FULL, sr.y, l);
+      s4.z = __shfl_sync(FULL, sr.z, l); s4.w = __shfl_sync(FULL, sr.w, l);
+      u64 sum;
+      u32 L;
+      nbr_components_warp<SM, UF>(g, tt, s4, sum, L, bytes);
+      if (lane == l) finish(tt, s4, sum, L);
+    }
+  };
   for (u32 w0 = wrank; w0 < nwords; w0 += U * wsize) {
     u32 bits[U];
     uint4 sr[U];
+    u32 tid[U];
 #pragma unroll
-    for (u32 j = 0; j < U; j++) {          // bitmap words and score records, all in flight
-      const u32 w = w0 + j * wsize, t = w * 32 + lane;
-      bits[j] = w < nwords ? g.pool_word(w) : 0u;
-      sr[j] = t < cmd.n_ids ? g.srec(t) : make_uint4(0, 0, 0, 0);
+    for (u32 j = 0; j < U; j++) {          // bitmap words (pool slots) and score records, all in flight
+      const u32 w = w0 + j * wsize;
+      if constexpr (BM) {
+        tid[j] = w * 32 + lane;
+        bits[j] = w < nwords ? g.pool_word(w) : 0u;
+      } else {
+        const u32 i = w * 32 + lane;
+        tid[j] = i < cmd.pool_size ? g.pool_ids(i) : NONE;
+        bits[j] = __ballot_sync(FULL, tid[j] != NONE);
+      }
+    }
+#pragma unroll
+    for (u32 j = 0; j < U; j++) {
+      const bool ok = BM ? tid[j] < cmd.n_ids : tid[j] != NONE;
+      sr[j] = ok ? g.srec(tid[j]) : make_uint4(0, 0, 0, 0);
+    }
+    if constexpr (NBR) {                       // evicted neighbours: deferred (all lanes converged here)
+#pragma unroll
+      for (u32 j = 0; j < U; j++) {
+        const bool slow = ((bits[j] >> lane) & 1u) && sr[j].w != 0;
+        const u32 m = __ballot_sync(FULL, slow);
+        if (slow) wq[nq + __popc(m & ((1u << lane) - 1))] = tid[j];
+        nq += __popc(m);
+      }
     }
 #pragma unroll
     for (u32 j = 0; j < U; j++) {
       const bool in = (bits[j] >> lane) & 1u;
-      Cand c;
-      c.id = (w0 + j * wsize) * 32 + lane;
+      const u32 id = tid[j];
       if constexpr (NBR) {
-        const bool slow = in && sr[j].w != 0;    // evicted neighbours: phase 2
-        const u32 m = __ballot_sync(FULL, slow);
-        if (m) {
-          u32 at = 0;
-          if (lane == 0) at = atomicAdd(slown, (u32)__popc(m));
-          at = __shfl_sync(FULL, at, 0);
-          if (slow) g.m.w(g.L.slowq + at + __popc(m & ((1u << lane) - 1))) = c.id;
-        }
-        if (!in || slow) continue;
+        if (!in || sr[j].w != 0) continue;
         evals++;
-        bytes += 16;
+        bytes += BM ? 16 : 20;                 // score record (+ pool slot)
         if constexpr (H == H_ABL) {
+          Cand c;
+          c.id = id;
           abl_finish(abl_c(cmd.heur) == ABL_NO ? 1ull : (u64)sr[j].y, sr[j].x, sr[j].z, cmd, c);
+          cand_take(best, bk, c);
         } else {
-          stale_score((u64)sr[j].y, sr[j].x, sr[j].z, cmd.clock, c.num, c.den);
+          const u32 k = stale_key(sr[j].y, sr[j].x, sr[j].z, clock1);
+          const bool clear = k + KEY_MARGIN < bk;
+          if (clear || (bk != KEY_NONE && k <= bk + KEY_MARGIN)) {   // new best, or a near-tie: exact
+            Cand c;
+            c.id = id;
+            stale_score((u64)sr[j].y, sr[j].x, sr[j].z, cmd.clock, c.num, c.den);
+            if (clear || cand_less(c, best)) { best = c; bk = k; }
+          }
         }
       } else {
         if (!in) continue;
+        Cand c;
+        c.id = id;
         evals++;
+        if constexpr (!BM) bytes += 4;         // pool slot
         if constexpr (H == H_LRU) {
           stale_score(1, 1, sr[j].z, cmd.clock, c.num, c.den);
           bytes += 4;
@@ -563,51 +731,22 @@ __device__ __forceinline__ void score_bm(const Sim<false> &g, const Cmd &cmd, u3
           c.num = splitmix64(cmd.seed ^ (cmd.decisions << 32) ^ (u64)c.id); c.den = 1;
           bytes += 4;
         }
+        cand_take(best, bk, c, int_key_heur(H));
       }
-      cand_take(best, bk, c, int_key_heur(H));
+    }
+    if constexpr (NBR) {
+      __syncwarp();
+      while (nq >= 32) {                       // a full round of slow candidates: one per lane
+        const u32 t = wq[nq - 32 + lane];
+        nq -= 32;
+        __syncwarp();
+        resolve(t);
+      }
     }
   }
   if constexpr (NBR) {
-    cg::this_grid().sync();
-    // phase 2: warp w takes queue entries [32 w, 32 w + 32), [32 (w + W), ...):
-    // one candidate per lane (phased gathers); degree > NB: the whole warp
-    const u32 ns = __ldcg(slown);
-    constexpr bool UF = H != H_DTR;
-    for (u32 i0 = wrank * 32; i0 < ns; i0 += wsize * 32) {
-      const u32 i = i0 + lane;
-      const u32 t = i < ns ? __ldcg(&g.m.w(g.L.slowq + i)) : NONE;
-      uint4 sr = make_uint4(0, 0, 0, 0), ar = make_uint4(0, 0, 0, 0);
-      if (t != NONE) { sr = g.srec(t); ar = g.arec(t); }
-      const bool big = t != NONE && ar.y + ar.w > NB;
-      auto finish = [&](u32 tt, const uint4 &s4, u64 sum, u32 L) {
-        Cand c;
-        c.id = tt;
-        evals++;
-        bytes += 16;
-        if constexpr (H == H_ABL) abl_finish((u64)s4.y + sum, s4.x, s4.z, cmd, c);
-        else stale_score((u64)s4.y + sum, s4.x, L, cmd.clock, c.num, c.den);
-        cand_take(best, bk, c);
-      };
-      if (t != NONE && !big) {
-        u64 sum;
-        u32 L;
-        nbr_components_phased<false, UF>(g, sr, ar, sum, L, bytes);
-        finish(t, sr, sum, L);
-      }
-      u32 bm = __ballot_sync(FULL, big);
-      while (bm) {
-        const u32 l = __ffs(bm) - 1;
-        bm &= bm - 1;
-        const u32 tt = __shfl_sync(FULL, t, l);
-        uint4 s4;
-        s4.x = __shfl_sync(FULL, sr.x, l); s4.y = __shfl_sync(FULL, sr.y, l);
-        s4.z = __shfl_sync(FULL, sr.z, l); s4.w = __shfl_sync(FULL, sr.w, l);
-        u64 sum;
-        u32 L;
-        nbr_components_warp<UF>(g, tt, s4, sum, L, bytes);
-        if (lane == l) finish(tt, s4, sum, L);
-      }
-    }
+    __syncwarp();
+    if (nq) resolve(lane < nq ? wq[lane] : NONE);
   }
 }
 
@@ -663,6 +802,7 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
     // to the whole warp (msps_closure)
     const u32 FULL = 0xffffffffu, n = BM ? cmd.n_ids : cmd.pool_size;
     const bool down = cmd.heur != H_MSPS;
+    const bool use_cc = g.L.ccache && cmd.n_ev != NONE;
     auto finish = [&](u32 t, const uint4 &sr, u64 sum) {
       Cand c;
       c.id = t;
@@ -678,23 +818,48 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
       evals++;
       cand_take(best, bk, c);
     };
-    for (u32 base = wrank * 32; base < n; base += nw * 32) {
-      const u32 i = base + lane;
-      u32 t = NONE;
-      if (i < n) {
-        if constexpr (BM) { if (g.in_pool(i)) t = i; }
-        else t = g.pool_ids(i);
+    constexpr u32 U = SM ? 1 : 4;            // global-memory state: four chunks' loads in flight per lane
+    for (u32 base = wrank * 32; base < n; base += U * nw * 32) {
+      u32 tj[U];
+      uint4 srj[U];
+      uint2 ccj[U];
+#pragma unroll
+      for (u32 j = 0; j < U; j++) {
+        const u32 i = base + j * nw * 32 + lane;
+        tj[j] = NONE;
+        if (i < n) {
+          if constexpr (BM) { if (g.in_pool(i)) tj[j] = i; }
+          else tj[j] = g.pool_ids(i);
+        }
       }
-      uint4 sr = make_uint4(0, 0, 0, 0);
-      if (t != NONE) sr = g.srec(t);
+#pragma unroll
+      for (u32 j = 0; j < U; j++) srj[j] = tj[j] != NONE ? g.srec(tj[j]) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (u32 j = 0; j < U; j++) ccj[j] = use_cc && srj[j].w ? g.ccache(tj[j]) : make_uint2(0, 0);
+#pragma unroll
+      for (u32 j = 0; j < U; j++) {
+      const u32 t = tj[j];
+      const uint4 sr = srj[j];
       bool ok = true;
       u64 sum = 0;
       if (t != NONE && sr.w) {                 // nev = 0: no evicted neighbour, the closure is empty
-        const uint4 ar = g.arec(t);
-        u64 up = 0, dn = 0, b = 0;
-        ok = closure_lane<SM, false>(g, t, ar, up, b) && (!down || closure_lane<SM, true>(g, t, ar, dn, b));
-        if (ok) { sum = up + dn; bytes += b; }
-        bytes += 16;                           // adjacency record
+        // cached halves {up+1, down+1} (0 = stale), else walked and stored
+        const uint2 cc = ccj[j];
+        u64 up = cc.x ? cc.x - 1u : 0, dn = cc.y ? cc.y - 1u : 0, b = 0;
+        const bool wu = !cc.x, wd = down && !cc.y;
+        if (use_cc) bytes += 8;
+        PROF_ADD(16, (wu || wd) ? 0 : 1);
+        PROF_ADD(17, (wu || wd) ? 1 : 0);
+        if (wu || wd) {
+          const uint4 ar = g.arec(t);
+          ok = (!wu || closure_lane<SM, false>(g, t, ar, up, b)) && (!wd || closure_lane<SM, true>(g, t, ar, dn, b));
+          if (ok) {
+            bytes += b;
+            if (use_cc) g.ccache(t) = make_uint2((u32)up + 1u, down ? (u32)dn + 1u : 0u);
+          }
+          bytes += 16;                         // adjacency record
+        }
+        if (ok) sum = up + dn;
       }
       if (t != NONE && ok) finish(t, sr, sum);
       u32 ov = __ballot_sync(FULL, t != NONE && !ok);
@@ -712,9 +877,15 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
           }
           slot = __shfl_sync(FULL, slot, 0);
         }
-        const u64 s2 = msps_closure(g, g.arec(tt), slot, msps_tail + (threadIdx.x >> 5), bytes, tt, down);
+        u64 u2 = 0;
+        if (lane == 0) PROF_ADD(18, 1);
+        const u64 s2 = msps_closure(g, g.arec(tt), slot, msps_tail + (threadIdx.x >> 5), bytes, tt, down, &u2);
         if (locked && lane == 0) { __threadfence(); atomicExch(&g.m.w(g.L.msps_lock + slot), 0u); }
-        if (lane == l) finish(tt, sr, s2);
+        if (lane == l) {
+          if (use_cc) g.ccache(tt) = make_uint2((u32)u2 + 1u, down ? (u32)(s2 - u2) + 1u : 0u);
+          finish(tt, sr, s2);
+        }
+      }
       }
     }
   }
@@ -725,7 +896,7 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
 // WIDE: global-memory team (four candidates in flight per thread, else two).
 template <bool SM, bool BM, bool WIDE = false, bool CL = true>
 __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, u32 wrank, u32 wsize,
-                           volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk, u32 *slown = nullptr) {
+                           volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk, u32 *wq = nullptr) {
   Cand best = cand_none();
   bk = KEY_NONE;
   if (BM && rank == 0) bytes += (cmd.n_ids + 7) / 8;     // the pool bitmap
@@ -738,15 +909,15 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
   constexpr u32 K = WIDE ? 4 : 2;
   if constexpr (!SM && BM) {
     switch (cmd.heur) {
-      case H_DTR: score_bm<H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_DTR_EQ: score_bm<H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_LRU: score_bm<H_LRU, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_SIZE: score_bm<H_SIZE, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_LOCAL: score_bm<H_LOCAL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
-      case H_RANDOM: score_bm<H_RANDOM, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown); return best;
+      case H_DTR: score_stream<false, true, H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
+      case H_DTR_EQ: score_stream<false, true, H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
+      case H_LRU: score_stream<false, true, H_LRU, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
+      case H_SIZE: score_stream<false, true, H_SIZE, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
+      case H_LOCAL: score_stream<false, true, H_LOCAL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
+      case H_RANDOM: score_stream<false, true, H_RANDOM, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
       default:
         if (is_abl(cmd.heur) && abl_c(cmd.heur) != ABL_ESTAR) {
-          score_bm<H_ABL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, slown);
+          score_stream<false, true, H_ABL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq);
           return best;
         }
         break;
@@ -756,6 +927,12 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
     const u64 kmin = team_intkey_min(g, cmd, rank, size, bytes, evals);
     if (kmin != ~0ull) { best = intkey_cand(g, cmd, kmin); bk = cand_key(best, true); }
     return best;
+  }
+  if constexpr (!SM) {   // state in global memory (CTA engine): the stream pass with its slow stack
+    if (wq) {
+      if (cmd.heur == H_DTR) { score_stream<false, false, H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best; }
+      if (cmd.heur == H_DTR_EQ) { score_stream<false, false, H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best; }
+    }
   }
   switch (cmd.heur) {
     case H_DTR: score_loop<SM, H_DTR, K>(g, cmd, rank, size, best, bk, bytes, evals); return best;

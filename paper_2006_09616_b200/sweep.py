@@ -89,28 +89,30 @@ class RankSweep:
         return torch.cat([b.rows for b in self.batches]) if self.batches else None
 
 
-def gather_rows(local_rows_u8, n_local, max_local, world_size, group=None):
-    """all_gather_into_tensor of fixed-size row tables (padded to max_local rows);
-    returns the concatenated table as a numpy structured array (valid rows only)."""
+def gather_rows(local_rows_u8, counts, world_size, group=None):
+    """ONE all_gather_into_tensor of fixed-size row tables (each rank's padded to
+    max(counts) rows).  counts[r] = rank r's number of cells -- every rank knows
+    them from the deterministic shard(), so no collective is spent on them.
+    Returns the concatenated table as a numpy structured array (valid rows only)."""
     import torch
     import torch.distributed as dist
     rb = RESULT_DTYPE.itemsize
     dev = local_rows_u8.device
+    max_local = max(max(counts), 1)
+    rank = dist.get_rank(group) if world_size > 1 else 0
+    n_local = int(counts[rank])
     padded = torch.zeros(max_local * rb, dtype=torch.uint8, device=dev)
     if n_local:
         padded[: n_local * rb] = local_rows_u8[: n_local * rb]
-    counts = torch.tensor([n_local], dtype=torch.int64, device=dev)
-    all_counts = torch.zeros(world_size, dtype=torch.int64, device=dev)
-    out = torch.zeros(world_size * max_local * rb, dtype=torch.uint8, device=dev)
     if world_size > 1:
-        dist.all_gather_into_tensor(all_counts, counts, group=group)
+        if dev.type == "cuda" and dist.get_backend(group) == "gloo":
+            padded = padded.cpu()            # gloo gathers host tensors (CPU tests, world-2 GPU test)
+        out = torch.empty(world_size * max_local * rb, dtype=torch.uint8, device=padded.device)
         dist.all_gather_into_tensor(out, padded, group=group)
     else:
-        all_counts.copy_(counts)
-        out.copy_(padded)
+        out = padded
     table = out.cpu().numpy().view(RESULT_DTYPE).reshape(world_size, max_local)
-    cnt = all_counts.cpu().numpy()
-    return np.concatenate([table[r, : int(cnt[r])] for r in range(world_size)])
+    return np.concatenate([table[r, : int(counts[r])] for r in range(world_size)])
 
 
 def order_by_cell(rows):
@@ -129,6 +131,5 @@ def run_sweep(logs, log_views, cells, rank=0, world_size=1, device=None, group=N
     local = rs.rows_device()
     if local is None:
         local = torch.zeros(0, dtype=torch.uint8, device=device or "cuda")
-    max_local = max(len(s) for s in shards)
-    rows = gather_rows(local, len(mine), max(max_local, 1), world_size, group)
+    rows = gather_rows(local, [len(s) for s in shards], world_size, group)
     return order_by_cell(rows)

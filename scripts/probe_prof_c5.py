@@ -14,7 +14,7 @@ w = models.CONFIG_MODELS[m]()
 v = LogView(w)
 s = dict(log=0, budget=v.budget(pm), heuristic=P.HEURISTICS[h], thrash_kill=16, max_decisions=cap)
 b = P.DeviceBatch([w], [s], engine=P.ENGINE_CTA)
-buf = np.zeros(16, np.uint64)
+buf = np.zeros(32, np.uint64)
 P.lib.dtr_debug_profile(buf.ctypes.data, 1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); b.run(); e1.record(); torch.cuda.synchronize()
@@ -28,4 +28,7 @@ print(f"{m} {h} pm={pm} n={v.n} dec={d} remats={int(r['remats'])} st={int(r['sta
       f"x{buf[3]}  cta-team={buf[4] / max(buf[5], 1):.0f} x{buf[5]}  init={buf[6]}\n"
       f"  rec+evict {buf[8] / max(buf[9], 1):.0f} x{buf[9] / max(d, 1):.2f}/dec, complete_top {buf[10] / max(buf[11], 1):.0f} "
       f"x{buf[11] / max(d, 1):.2f}/dec, lock/push {buf[12] / max(buf[13], 1):.0f} x{buf[13] / max(d, 1):.2f}/dec, "
-      f"loop iters {buf[14] / max(d, 1):.2f}/dec", flush=True)
+      f"loop iters {buf[14] / max(d, 1):.2f}/dec\n"
+      f"  closure cache: hits {buf[16] / max(d, 1):.1f}/dec, lane walks {buf[17] / max(d, 1):.1f}/dec, "
+      f"warp BFS {buf[18] / max(d, 1):.2f}/dec, events {buf[19] / max(d, 1):.2f}/dec, "
+      f"event-walk nodes {buf[20] / max(d, 1):.1f}/dec, event cycles {buf[21] / max(d, 1):.0f}/dec", flush=True)

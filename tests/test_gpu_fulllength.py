@@ -1,0 +1,82 @@
+"""Full-length parity on the paper-shaped logs (VERDICT r1 "Next round" #2).
+
+Every row of tests/golden/c5_fulllength.json was written by
+scripts/make_golden_runs.py, which runs oracle/ ONLY (no CUDA-path code):
+the config-5 sweep cells (6 models x 30 budget ratios x {h_DTR, h_DTR_eq,
+LRU, size, MSPS}) and the config-4 long logs, each replayed to its
+end (ok, OOM, or the thrash kill of reading C-13).  Here the CUDA path replays
+the same cells -- the config-5 ones as one sharded sweep (the launch
+configuration bench.py times), the config-4 ones on the whole-GPU engine --
+and every row field (status, clock, decisions, remats, computations, peak M,
+records done, FNV trace hash) must be identical.
+"""
+import json
+import os
+
+import pytest
+
+from dtr_inputs import LogView, models
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "c5_fulllength.json")
+FIELDS = ("status", "records_done", "clock", "base", "decisions", "remats", "computations", "peak_M", "trace_hash")
+
+
+def _rows():
+    if not os.path.exists(GOLD):
+        pytest.skip("no golden full-length rows")
+    return json.load(open(GOLD))["rows"]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2006_09616_b200 as P
+    return P
+
+
+def test_config5_full_sweep_vs_oracle(P):
+    from paper_2006_09616_b200 import sweep
+    gold = [r for r in _rows() if r["model"] in models.CONFIG_MODELS]
+    names = sorted({r["model"] for r in gold})
+    logs = [models.CONFIG_MODELS[m]() for m in names]
+    views = [LogView(w) for w in logs]
+    cells = []
+    for r in gold:
+        li = names.index(r["model"])
+        assert views[li].budget(r["permille"]) == r["budget"]
+        cells.append(dict(cell_id=len(cells), log=li, permille=r["permille"], budget=r["budget"],
+                          heuristic=P.HEURISTICS[r["heuristic"]], thrash_kill=r["thrash_kill"], max_decisions=0))
+    rows = sweep.run_sweep(logs, views, cells)
+    bad = []
+    for r, g in zip(gold, rows):
+        for f in FIELDS:
+            if int(g[f]) != int(r[f]):
+                bad.append((r["model"], r["heuristic"], r["permille"], f, int(g[f]), int(r[f])))
+    assert not bad, bad[:20]
+    print(f"{len(gold)} full-length cells identical, {sum(r['decisions'] for r in gold)} decisions")
+
+
+@pytest.mark.parametrize("model", ["lstm4096", "transformer512"])
+def test_config4_full_run_vs_oracle(P, model):
+    gold = [r for r in _rows() if r["model"] == model]
+    if not gold:
+        pytest.skip(f"no golden rows for {model}")
+    w = models.lstm(T=4096, layers=2) if model == "lstm4096" else models.transformer(layers=512)
+    v = LogView(w)
+    specs = []
+    for r in gold:
+        assert r["budget"] == v.peak_total * 100000 // v.n
+        specs.append(dict(log=0, budget=r["budget"], heuristic=P.HEURISTICS[r["heuristic"]],
+                          thrash_kill=r["thrash_kill"]))
+    for r, s in zip(gold, specs):
+        b = P.DeviceBatch([w], [s], engine=P.ENGINE_GRID)
+        b.run()
+        import torch
+        torch.cuda.synchronize()
+        g = b.result_rows()[0]
+        for f in FIELDS:
+            assert int(g[f]) == int(r[f]), (model, r["heuristic"], f, int(g[f]), int(r[f]))
+        del b

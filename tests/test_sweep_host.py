@@ -66,8 +66,8 @@ def _worker(rank, ws, port, out_q):
         rows[i]["clock"] = 1000 + c["cell_id"]
         rows[i]["decisions"] = rank
     local = torch.from_numpy(rows.view(np.uint8).copy())
-    max_local = max(len(s) for s in sweep.shard(cells, views, ws))
-    table = sweep.order_by_cell(sweep.gather_rows(local, len(mine), max_local, ws))
+    counts = [len(s) for s in sweep.shard(cells, views, ws)]
+    table = sweep.order_by_cell(sweep.gather_rows(local, counts, ws))
     out_q.put((rank, table["cell_id"].tolist(), table["clock"].tolist(), table["decisions"].tolist()))
     dist.destroy_process_group()
 
