@@ -159,6 +159,14 @@ int dtr_version(void);
 int dtr_batch_workspace_bytes(const uint32_t *dims, uint32_t n_cells, uint32_t engine,
                               uint64_t *bytes_out);
 
+/* Shared-memory class of one CTA-engine cell (dims {n_tensors, n_edges,
+ * heuristic} as above): 0 = small (several CTAs per SM), 1 = staged whole in
+ * shared memory, 2 = state in the global workspace.  dtr_replay_batch makes
+ * one launch per run of consecutive cells of one class, so a caller that
+ * orders its cells (e.g. longest first, sweep.RankSweep) keeps each class
+ * contiguous.  Host only, no device call.  Returns DTR_OK or DTR_E_INVAL. */
+int dtr_cta_class(uint32_t n_tensors, uint32_t n_edges, uint32_t heuristic, uint32_t *class_out);
+
 /* Replay every cell.  d_words: device, packed logs.  d_cells: device, n_cells
  * dtr_cell.  h_dims: HOST copy of the dims array above (sizes the workspace
  * and the shared-memory staging of each launch).  d_ws: device workspace of

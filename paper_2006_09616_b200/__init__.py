@@ -5,9 +5,9 @@ this thin ctypes binding. There is no CPU fallback: importing fails loudly if
 the library is missing.
 """
 from .binding import (lib, Runtime, DeviceBatch, AdversaryBatch, ADV_DTYPE, abl_id, DEALLOC, replay_batch, replay_batch_host, pack_logs, make_cells,
-                      cell_dims, workspace_bytes, DtrError, HEURISTICS, ENGINE_CTA, ENGINE_GRID, STATUS_NAMES,
+                      cell_dims, workspace_bytes, cta_class, DtrError, HEURISTICS, ENGINE_CTA, ENGINE_GRID, STATUS_NAMES,
                       TRACE_DTYPE, RESULT_DTYPE, CELL_DTYPE, EXPORTS)
 
 __all__ = ["lib", "Runtime", "DeviceBatch", "AdversaryBatch", "ADV_DTYPE", "abl_id", "DEALLOC", "replay_batch", "replay_batch_host", "pack_logs", "make_cells",
-           "cell_dims", "workspace_bytes", "DtrError", "HEURISTICS", "ENGINE_CTA", "ENGINE_GRID",
+           "cell_dims", "workspace_bytes", "cta_class", "DtrError", "HEURISTICS", "ENGINE_CTA", "ENGINE_GRID",
            "STATUS_NAMES", "TRACE_DTYPE", "RESULT_DTYPE", "CELL_DTYPE", "EXPORTS"]

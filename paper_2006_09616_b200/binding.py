@@ -51,7 +51,7 @@ assert TRACE_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 96 and CELL_DTYPE
 assert ADV_DTYPE.itemsize == 40
 
 # every symbol include/dtr.h declares
-EXPORTS = ["dtr_strerror", "dtr_last_cuda_error", "dtr_version", "dtr_batch_workspace_bytes",
+EXPORTS = ["dtr_strerror", "dtr_last_cuda_error", "dtr_version", "dtr_batch_workspace_bytes", "dtr_cta_class",
            "dtr_replay_batch", "dtr_replay_batch_host", "dtr_create", "dtr_destroy", "dtr_compute", "dtr_get",
            "dtr_release", "dtr_rematerialize", "dtr_ensure", "dtr_stats", "dtr_trace", "dtr_debug_evict",
            "dtr_debug_set_budget", "dtr_debug_scores", "dtr_pool_argmin", "dtr_adversary_workspace_bytes",
@@ -83,6 +83,8 @@ def _load():
     L.dtr_version.restype = i32
     L.dtr_batch_workspace_bytes.restype = i32
     L.dtr_batch_workspace_bytes.argtypes = [P, u32, u32, C.POINTER(u64)]
+    L.dtr_cta_class.restype = i32
+    L.dtr_cta_class.argtypes = [u32, u32, u32, C.POINTER(u32)]
     L.dtr_replay_batch.restype = i32
     L.dtr_replay_batch.argtypes = [P, P, P, u32, u32, P, u64, P, P, P]
     L.dtr_pool_argmin.restype = i32
@@ -179,6 +181,13 @@ def workspace_bytes(dims, engine):
     return out.value
 
 
+def cta_class(n_tensors, n_edges, heuristic):
+    """Shared-memory class (0 small, 1 staged, 2 global) of a CTA-engine cell."""
+    out = C.c_uint32(0)
+    _check(lib.dtr_cta_class(int(n_tensors), int(n_edges), int(heuristic), C.byref(out)), "dtr_cta_class")
+    return out.value
+
+
 def replay_batch(d_words, d_cells, h_dims, n_cells, engine, d_ws, ws_bytes, d_rows, d_trace, stream):
     """dtr_replay_batch on device pointers (ints) with host dims (np.uint32),
     asynchronous on `stream` (int handle)."""
@@ -222,6 +231,16 @@ class DeviceBatch:
         self.trace = torch.zeros(max(ttot, 1) * TRACE_DTYPE.itemsize, dtype=torch.uint8, device=dev) if ttot else None
         self.h_cells = cells
         self.h_words = words
+        self.specs = specs
+
+    def launches_per_run(self):
+        """Kernel launches one run() makes: grid engine one per cell; CTA engine one
+        per run of consecutive cells of one shared-memory class (dtr.cu)."""
+        if self.engine == ENGINE_GRID:
+            return self.n_cells
+        d = self.h_dims.reshape(-1, 3)
+        cls = [cta_class(int(a), int(b), int(c)) for a, b, c in d]
+        return sum(1 for i in range(len(cls)) if i == 0 or cls[i] != cls[i - 1])
 
     def run(self, stream=None):
         s = stream if stream is not None else self.torch.cuda.current_stream(self.device)

@@ -4,6 +4,14 @@
 // through the launchers declared in kcommon.cuh.
 #include "kcommon.cuh"
 #include <mutex>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges show up in nsys / ncu --nvtx, no-ops otherwise
+
+namespace {
+struct NvtxRange {   // one range per host entry point (RAII: every return path pops it)
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 using namespace dtr;
 
@@ -62,6 +70,17 @@ int dtr_batch_workspace_bytes(const uint32_t *dims, uint32_t n_cells, uint32_t e
     else cur += b;
   }
   *bytes_out = engine == DTR_ENGINE_GRID ? cur + mx : cur;
+  return DTR_OK;
+}
+
+static int cta_class_of(u32 n, u32 E, u32 heur) {
+  const u64 s = cta_smem_need(n, E, heur);
+  return s <= 48 * 1024 - 1024 ? 0 : (s <= CTA_SMEM_MAX ? 1 : 2);
+}
+
+int dtr_cta_class(uint32_t n_tensors, uint32_t n_edges, uint32_t heuristic, uint32_t *class_out) {
+  if (!class_out || !valid_heuristic(heuristic)) return DTR_E_INVAL;
+  *class_out = (uint32_t)cta_class_of(n_tensors, n_edges, heuristic);
   return DTR_OK;
 }
 
@@ -133,6 +152,7 @@ static int grid_blocks(int *blocks) {
 int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uint32_t *h_dims, uint32_t n_cells,
                      uint32_t engine, void *d_ws, uint64_t ws_bytes, dtr_result *d_rows, dtr_evict_rec *d_trace,
                      void *stream) {
+  NvtxRange nvtx_range("dtr_replay_batch");
   if (!n_cells) return DTR_OK;
   if (!d_words || !d_cells || !h_dims || !d_ws || !d_rows) return DTR_E_INVAL;
   if (engine != DTR_ENGINE_CTA && engine != DTR_ENGINE_GRID) return DTR_E_INVAL;
@@ -151,9 +171,8 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
     if (rc) return rc;
     const int sm_count = ds->sm_count;
     auto cls_of = [&](u32 i, u64 *need) -> int {
-      u64 s = cta_smem_need(h_dims[3 * i], h_dims[3 * i + 1], h_dims[3 * i + 2]);
-      *need = s;
-      return s <= 48 * 1024 - 1024 ? 0 : (s <= CTA_SMEM_MAX ? 1 : 2);
+      *need = cta_smem_need(h_dims[3 * i], h_dims[3 * i + 1], h_dims[3 * i + 2]);
+      return cta_class_of(h_dims[3 * i], h_dims[3 * i + 1], h_dims[3 * i + 2]);
     };
     bool used[3] = {false, false, false};
     u64 first_need;
@@ -208,6 +227,7 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
 }
 
 int dtr_pool_argmin(const uint32_t *d_log, uint32_t heuristic, void *d_ws, uint64_t *d_out, void *stream) {
+  NvtxRange nvtx_range("dtr_pool_argmin");
   if (!d_log || !d_ws || !d_out || !valid_heuristic(heuristic)) return DTR_E_INVAL;
   DevState *ds;
   int rc = dev_state(&ds);
@@ -221,6 +241,7 @@ int dtr_pool_argmin(const uint32_t *d_log, uint32_t heuristic, void *d_ws, uint6
 int dtr_replay_batch_host(const uint32_t *h_words, uint64_t n_words, const dtr_cell *h_cells, uint32_t n_cells,
                           uint32_t engine, dtr_result *h_rows, dtr_evict_rec *h_trace, uint64_t trace_total,
                           void *stream) {
+  NvtxRange nvtx_range("dtr_replay_batch_host");
   if (!n_cells) return DTR_OK;
   if (!h_words || !h_cells || !h_rows) return DTR_E_INVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -294,6 +315,7 @@ int dtr_adversary_workspace_bytes(const dtr_adversary *h_runs, uint32_t n_runs, 
 int dtr_adversary_batch(const dtr_adversary *d_runs, const dtr_adversary *h_runs, uint32_t n_runs, void *d_ws,
                         uint64_t ws_bytes, dtr_result *d_rows, uint32_t *d_parents, dtr_evict_rec *d_trace,
                         void *stream) {
+  NvtxRange nvtx_range("dtr_adversary_batch");
   if (!d_runs || !h_runs || !d_rows || !d_parents || (n_runs && !d_ws)) return DTR_E_INVAL;
   if (n_runs == 0) return DTR_OK;
   uint64_t need = 0;

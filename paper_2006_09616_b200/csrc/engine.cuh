@@ -199,17 +199,19 @@ extern __shared__ __align__(16) u32 g_smem[];
 template <bool SM>
 struct Mem {
   u32 *gbase;
+  // SM = false: gbase is a global-memory pointer; telling the compiler so lets
+  // it emit LDG/STG (global) instead of generic LD/ST
   __device__ __forceinline__ u32 &w(u32 off) const {
     if constexpr (SM) return g_smem[off];
-    else return gbase[off];
+    else { __builtin_assume(__isGlobal(gbase)); return gbase[off]; }
   }
   __device__ __forceinline__ uint4 &q(u32 off) const {   // off multiple of 4
     if constexpr (SM) return reinterpret_cast<uint4 *>(g_smem)[off >> 2];
-    else return reinterpret_cast<uint4 *>(gbase)[off >> 2];
+    else { __builtin_assume(__isGlobal(gbase)); return reinterpret_cast<uint4 *>(gbase)[off >> 2]; }
   }
   __device__ __forceinline__ uint2 &d(u32 off) const {   // off multiple of 2
     if constexpr (SM) return reinterpret_cast<uint2 *>(g_smem)[off >> 1];
-    else return reinterpret_cast<uint2 *>(gbase)[off >> 1];
+    else { __builtin_assume(__isGlobal(gbase)); return reinterpret_cast<uint2 *>(gbase)[off >> 1]; }
   }
 };
 

@@ -50,7 +50,8 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   if (tid == 0) PROF_ADD(6, ti1 - ti0);
   u64 bytes = 0, evals = 0;
   // global-memory state: the dynamic shared memory holds the per-warp slow stacks (score_stream)
-  u32 *wq = SM ? nullptr : g_smem + warp * SLOWQ;
+  const SlowStack wq = SM ? SlowStack{nullptr, 0}
+                          : SlowStack{reinterpret_cast<uint2 *>(g_smem) + warp * CTA_WQ_PAIRS, CTA_WQ_PAIRS};
   if (warp == 0) {
     Leader<SM, false> L;
     if (lane == 0) leader_init(L, g, logw, cell, trace);
@@ -88,11 +89,12 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
         continue;
       }
       PROF_T(t5);
-      if (lane == 0) sh.cmd = c;
+      if (lane == 0) { sh.cmd = c; sh.best = KEY_NONE; }
       __syncthreads();
       if (c.kind != CMD_ARGMIN) break;
       u32 bk;
-      Cand best = team_score<SM, false, false, CL>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk, wq);
+      Cand best = team_score<SM, false, false, CL>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk, wq,
+                                                   &sh.best);
       best = block_argmin(best, bk, sh.red, int_key_heur(c.heur));
       PROF_T(t6);
       if (lane == 0) { res = best; have = true; PROF_ADD(4, t6 - t5); PROF_ADD(5, 1); }
@@ -104,7 +106,8 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
       const Cmd c = sh.cmd;
       if (c.kind != CMD_ARGMIN) break;
       u32 bk;
-      Cand best = team_score<SM, false, false, CL>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk, wq);
+      Cand best = team_score<SM, false, false, CL>(g, c, tid, blockDim.x, warp, blockDim.x >> 5, sh.msps_tail, bytes, evals, bk, wq,
+                                                   &sh.best);
       block_argmin(best, bk, sh.red, int_key_heur(c.heur));
     }
   }

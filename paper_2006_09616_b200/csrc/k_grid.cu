@@ -12,7 +12,8 @@ struct __align__(16) GridShared {
   RedSmem red;
   ScanSmem scan;
   u32 msps_tail[GRID_THREADS / 32];
-  u32 wq[GRID_THREADS / 32][SLOWQ];   // per-warp stacks of deferred (slow) candidates
+  uint2 wq[GRID_THREADS / 32][GRID_WQ_PAIRS];   // per-warp stacks of deferred candidates
+  u32 best;                           // the block's best pass-1 key (score_stream pruning)
 };
 
 struct GridSync {
@@ -88,13 +89,14 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
       c.n_ids = __ldcg(&gcmd->n_ids);
       c.n_ev = __ldcg(&gcmd->n_ev);
       sh.cmd = c;
+      sh.best = KEY_NONE;
     }
     __syncthreads();
     if (sh.cmd.kind != CMD_ARGMIN) break;
     u32 bk;
     PROF_T(c0);
     Cand best = team_score<false, true, true>(g, sh.cmd, rank, size, wrank, wsize, sh.msps_tail, bytes, evals, bk,
-                                              sh.wq[tid >> 5]);
+                                              SlowStack{sh.wq[tid >> 5], GRID_WQ_PAIRS}, &sh.best);
     PROF_T(c1);
     const bool ik = int_key_heur(sh.cmd.heur);
     best = block_argmin(best, bk, sh.red, ik);
@@ -136,8 +138,8 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
 struct __align__(16) PaShared {
   RedSmem red;
   u32 msps_tail[PA_THREADS / 32];
-  u32 wq[PA_THREADS / 32][SLOWQ];
-  u32 last;
+  uint2 wq[PA_THREADS / 32][GRID_WQ_PAIRS];
+  u32 last, best;
 };
 
 __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *logw, u32 heur, char *ws,
@@ -157,8 +159,10 @@ __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *l
   const u32 rank = blockIdx.x * blockDim.x + tid, size = gridDim.x * blockDim.x;
   u64 bytes = 0, evals = 0;
   u32 bk;
+  if (tid == 0) sh.best = KEY_NONE;
+  __syncthreads();
   Cand best = team_score<false, true, true>(g, cmd, rank, size, rank >> 5, size >> 5, sh.msps_tail, bytes, evals, bk,
-                                            sh.wq[tid >> 5]);
+                                            SlowStack{sh.wq[tid >> 5], GRID_WQ_PAIRS}, &sh.best);
   const bool ik = int_key_heur(heur);
   best = block_argmin(best, bk, sh.red, ik);
   block_sum2(bytes, evals, sh.red);

@@ -41,7 +41,9 @@ using namespace dtr;
 #define WS_PARTIALS 512
 #define WS_PA_DONE 124       /* dtr_pool_argmin: blocks finished (u32; zeroed by the grid engine) */
 #define CTA_SMEM_MAX (225u * 1024u)
-#define CTA_WQ_BYTES (CTA_THREADS / 32 * SLOWQ * 4)   /* global-state cells: per-warp slow stacks (team.cuh) */  /* + ~1 KB static CtaShared <= 227 KB per block */
+#define CTA_WQ_PAIRS 1024u   /* global-state cells: per-warp stack of deferred candidates (team.cuh SlowStack) */
+#define CTA_WQ_BYTES (CTA_THREADS / 32 * CTA_WQ_PAIRS * 8)   /* = the dynamic shared memory of those launches */
+#define GRID_WQ_PAIRS 192u   /* whole-GPU teams: per-warp stack (>= 32 * 4 steps + 32) */  /* + ~1 KB static CtaShared <= 227 KB per block */
 
 // ---------------------------------------------------------------------------
 // Initialisation (team-parallel): static records and parents from the log,
@@ -230,6 +232,7 @@ struct __align__(16) CtaShared {
   RedSmem red;
   ScanSmem scan;
   u32 msps_tail[CTA_THREADS / 32];
+  u32 best;                          // the CTA team's best pass-1 key (score_stream pruning)
 };
 
 struct PercallArgs {

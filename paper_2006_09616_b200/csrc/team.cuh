@@ -599,33 +599,103 @@ __device__ __forceinline__ u32 stale_key(u32 c, u32 m, u32 L, u32 clock1) {
   return __float_as_uint(__fdividef(__uint2float_rn(c), __uint2float_rn(m) * __uint2float_rn(s)));
 }
 
-// Whole-GPU pass over the pool BITMAP (grid engine, dtr_pool_argmin).  Warp w
-// takes bitmap words w, w + W, w + 2W, ... (W = warps in the grid) and lane l
-// the id 32 * word + l, so each step reads one broadcast bitmap word and 32
-// consecutive score records (512 B, coalesced), U steps in flight per lane; a
-// candidate with nev = 0 is scored from its record alone (stale_key: no 64-bit
-// arithmetic unless it is a new best or a near-tie).  A candidate with evicted
-// neighbours is pushed on the warp's shared-memory stack `wq` (SLOWQ entries)
-// and resolved as soon as 32 are waiting -- one per lane, phased gathers
-// (nbr_components_phased); degree > NB: the whole warp (nbr_components_warp) --
-// and the rest after the stream, so no grid barrier separates the two kinds.
-constexpr u32 SLOWQ = 160;   // >= 31 + 4 steps x 32
+// Per-warp stack of deferred candidates in shared memory: (id, key of a LOWER
+// bound of its score) pairs.  e = null: no stack (the caller re-scans instead).
+struct SlowStack {
+  uint2 *e;
+  u32 cap;   // pairs; >= 32 * U + 32 where it is used
+};
 
+// Drain a warp's stack down to `keep` entries: first drop every entry whose
+// bound key exceeds `cur` (an exact score some candidate already has) by more
+// than KEY_MARGIN -- its exact score is higher, so it cannot be the argmin --
+// then resolve the rest from the top, 32 per round, one per lane
+// (resolve(NONE) = idle lane; resolve is warp-collective).
+template <class R>
+__device__ __forceinline__ void stack_drain(const SlowStack &st, u32 &nq, u32 keep, u32 cur, R resolve) {
+  const u32 FULL = 0xffffffffu, lane = threadIdx.x & 31;
+  u32 out = 0;
+  for (u32 i0 = 0; i0 < nq; i0 += 32) {      // compact the survivors to the front (order is irrelevant)
+    const u32 i = i0 + lane;
+    uint2 x = make_uint2(NONE, 0);
+    bool k = false;
+    if (i < nq) { x = st.e[i]; k = cur == KEY_NONE || !(x.y > cur + KEY_MARGIN); }
+    const u32 m = __ballot_sync(FULL, k);
+    if (k) st.e[out + __popc(m & ((1u << lane) - 1))] = x;   // writes never pass this chunk's reads
+    out += __popc(m);
+    __syncwarp();
+  }
+  nq = out;
+  while (nq > keep) {
+    u32 take = nq - keep;
+    take = take > 32 ? 32 : take;
+    const u32 t = lane < take ? st.e[nq - take + lane].x : NONE;
+    nq -= take;
+    __syncwarp();
+    resolve(t);
+  }
+}
+
+// The team's best key so far: the warp's, and (block team) the shared word
+// every warp lowers with atomicMin.  Any value is an exact score some
+// candidate has, so it is a safe pruning bound at any time.
+__device__ __forceinline__ u32 team_bound(u32 bk, u32 *sbest) {
+  u32 b = __reduce_min_sync(0xffffffffu, bk);
+  if (sbest) {
+    if ((threadIdx.x & 31) == 0) atomicMin(sbest, b);
+    const u32 s2 = *(volatile u32 *)sbest;
+    b = s2 < b ? s2 : b;
+  }
+  return b;
+}
+
+// Whole-GPU pass over the pool BITMAP (grid engine, dtr_pool_argmin).  Warp w
+// takes bitmap words w, w + W, w + 2W, ... (W = warps in the team) and lane l
+// the id 32 * word + l, so each step reads one broadcast bitmap word and 32
+// consecutive score records (512 B, coalesced), U steps in flight per lane.
 // BM = false: the same pass over the compact pool list (CTA engine with its
 // state in global memory): lane l of warp w takes pool slots 32 w + l,
-// 32 (w + W) + l, ...; the ids are a coalesced load and the score records a
-// gather, U steps in flight.
+// 32 (w + W) + l, ...; the ids are a coalesced load, the records a gather.
+//
+// Exact branch and bound.  A candidate with nev = 0 is scored from its record
+// alone (stale_key: no 64-bit arithmetic unless it is a new best or a
+// near-tie).  For a candidate with evicted neighbours the same record gives a
+// LOWER bound of its score: adjacent components only add cost to the numerator
+// and can only raise the max last access, which shortens the staleness
+// (h_DTR_eq and the EqClass ablation alike).  Such candidates are
+// pushed with their bound key on the warp's shared-memory stack; after the
+// stream (or when the stack runs full) the team's best key so far prunes them
+// (stack_drain: a bound above an exact score already found, by more than the
+// margin, cannot be the argmin -- a tie needs equality) and the survivors are
+// resolved 32 at a time, one per lane (phased gathers, nbr_components_phased;
+// degree > NB: the whole warp, nbr_components_warp).  sbest: a shared word of a
+// block-wide team (every thread of the block takes part; the caller resets it
+// to KEY_NONE before the barrier that starts the team: one barrier after the
+// stream lets every warp prune with the block's best), or null for a one-warp
+// team.
 template <bool SM, bool BM, int H, u32 U>
 __device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u32 wrank, u32 wsize, Cand &best,
-                                             u32 &bk, u64 &bytes, u64 &evals, u32 *wq) {
-  static_assert(U * 32 + 31 <= SLOWQ, "slow stack too small");
+                                             u32 &bk, u64 &bytes, u64 &evals, const SlowStack &st, u32 *sbest) {
   const u32 FULL = 0xffffffffu, lane = threadIdx.x & 31;
   const u32 nwords = BM ? (cmd.n_ids + 31) / 32 : (cmd.pool_size + 31) / 32;
   const u32 clock1 = (u32)(cmd.clock + 1);
   constexpr bool NBR = H == H_DTR || H == H_DTR_EQ || H == H_ABL;
   constexpr bool UF = H != H_DTR;
-  u32 nq = 0;                                  // warp-uniform stack depth
-  // resolve one slow candidate per lane (t = NONE: idle lane)
+  // neighbourhood-reading variant? (the ablation only for c = EqClass)
+  const bool nbr = NBR && (H != H_ABL || abl_c(cmd.heur) == ABL_EQCLASS);
+  // own-record score (exact for nev = 0; a lower bound otherwise): key, and the rational on demand
+  auto own_cand = [&](u32 id, const uint4 &r) {
+    Cand c;
+    c.id = id;
+    if constexpr (H == H_ABL) abl_finish(abl_c(cmd.heur) == ABL_NO ? 1ull : (u64)r.y, r.x, r.z, cmd, c);
+    else stale_score((u64)r.y, r.x, r.z, cmd.clock, c.num, c.den);
+    return c;
+  };
+  auto own_key = [&](const uint4 &r) -> u32 {
+    if constexpr (H == H_ABL) return cand_key(own_cand(0, r));
+    else return stale_key(r.y, r.x, r.z, clock1);
+  };
+  // one slow candidate per lane (NONE: idle lane)
   auto resolve = [&](u32 t) {
     uint4 sr = make_uint4(0, 0, 0, 0), ar = make_uint4(0, 0, 0, 0);
     if (t != NONE) { sr = g.srec(t); ar = g.arec(t); }
@@ -633,8 +703,6 @@ __device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u
     auto finish = [&](u32 tt, const uint4 &s4, u64 sum, u32 L) {
       Cand c;
       c.id = tt;
-      evals++;
-      bytes += BM ? 16 : 20;                   // score record (+ pool slot)
       if constexpr (H == H_ABL) abl_finish((u64)s4.y + sum, s4.x, s4.z, cmd, c);
       else stale_score((u64)s4.y + sum, s4.x, L, cmd.clock, c.num, c.den);
       cand_take(best, bk, c);
@@ -659,12 +727,12 @@ __device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u
       if (lane == l) finish(tt, s4, sum, L);
     }
   };
+  u32 nq = 0;                                  // warp-uniform stack depth
   for (u32 w0 = wrank; w0 < nwords; w0 += U * wsize) {
-    u32 bits[U];
+    u32 bits[U], tid[U];
     uint4 sr[U];
-    u32 tid[U];
 #pragma unroll
-    for (u32 j = 0; j < U; j++) {          // bitmap words (pool slots) and score records, all in flight
+    for (u32 j = 0; j < U; j++) {              // pool ids (bitmap words) and score records, all in flight
       const u32 w = w0 + j * wsize;
       if constexpr (BM) {
         tid[j] = w * 32 + lane;
@@ -680,43 +748,35 @@ __device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u
       const bool ok = BM ? tid[j] < cmd.n_ids : tid[j] != NONE;
       sr[j] = ok ? g.srec(tid[j]) : make_uint4(0, 0, 0, 0);
     }
-    if constexpr (NBR) {                       // evicted neighbours: deferred (all lanes converged here)
+    if constexpr (NBR) {
+      if (nbr) {                               // evicted neighbours: deferred with their bound key
 #pragma unroll
-      for (u32 j = 0; j < U; j++) {
-        const bool slow = ((bits[j] >> lane) & 1u) && sr[j].w != 0;
-        const u32 m = __ballot_sync(FULL, slow);
-        if (slow) wq[nq + __popc(m & ((1u << lane) - 1))] = tid[j];
-        nq += __popc(m);
+        for (u32 j = 0; j < U; j++) {
+          const bool slow = ((bits[j] >> lane) & 1u) && sr[j].w != 0;
+          const u32 m = __ballot_sync(FULL, slow);
+          if (slow) st.e[nq + __popc(m & ((1u << lane) - 1))] = make_uint2(tid[j], own_key(sr[j]));
+          nq += __popc(m);
+        }
       }
     }
 #pragma unroll
     for (u32 j = 0; j < U; j++) {
       const bool in = (bits[j] >> lane) & 1u;
       const u32 id = tid[j];
+      if (!in) continue;
+      evals++;
       if constexpr (NBR) {
-        if (!in || sr[j].w != 0) continue;
-        evals++;
         bytes += BM ? 16 : 20;                 // score record (+ pool slot)
-        if constexpr (H == H_ABL) {
-          Cand c;
-          c.id = id;
-          abl_finish(abl_c(cmd.heur) == ABL_NO ? 1ull : (u64)sr[j].y, sr[j].x, sr[j].z, cmd, c);
-          cand_take(best, bk, c);
-        } else {
-          const u32 k = stale_key(sr[j].y, sr[j].x, sr[j].z, clock1);
-          const bool clear = k + KEY_MARGIN < bk;
-          if (clear || (bk != KEY_NONE && k <= bk + KEY_MARGIN)) {   // new best, or a near-tie: exact
-            Cand c;
-            c.id = id;
-            stale_score((u64)sr[j].y, sr[j].x, sr[j].z, cmd.clock, c.num, c.den);
-            if (clear || cand_less(c, best)) { best = c; bk = k; }
-          }
+        if (nbr && sr[j].w != 0) continue;     // deferred
+        const u32 k = own_key(sr[j]);
+        const bool clear = k + KEY_MARGIN < bk;
+        if (clear || (bk != KEY_NONE && k <= bk + KEY_MARGIN)) {   // new best, or a near-tie: exact
+          const Cand c = own_cand(id, sr[j]);
+          if (clear || cand_less(c, best)) { best = c; bk = k; }
         }
       } else {
-        if (!in) continue;
         Cand c;
         c.id = id;
-        evals++;
         if constexpr (!BM) bytes += 4;         // pool slot
         if constexpr (H == H_LRU) {
           stale_score(1, 1, sr[j].z, cmd.clock, c.num, c.den);
@@ -736,17 +796,17 @@ __device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u
     }
     if constexpr (NBR) {
       __syncwarp();
-      while (nq >= 32) {                       // a full round of slow candidates: one per lane
-        const u32 t = wq[nq - 32 + lane];
-        nq -= 32;
-        __syncwarp();
-        resolve(t);
-      }
+      if (nq + 32 * U > st.cap) stack_drain(st, nq, st.cap / 2, team_bound(bk, sbest), resolve);   // make room
     }
   }
   if constexpr (NBR) {
-    __syncwarp();
-    if (nq) resolve(lane < nq ? wq[lane] : NONE);
+    if (!nbr) return;
+    u32 cur = team_bound(bk, sbest);
+    if (sbest) {                               // every warp's stream is in: prune with the block's best
+      __syncthreads();
+      cur = team_bound(bk, sbest);
+    }
+    stack_drain(st, nq, 0, cur, resolve);
   }
 }
 
@@ -785,108 +845,166 @@ __device__ __forceinline__ Cand intkey_cand(const Sim<SM> &g, const Cmd &cmd, u6
   return c;
 }
 
-// K5 pass: h_MSPS and the e* family (one candidate per lane, warp BFS on
-// frontier overflow).
+// K5 pass: h_MSPS and the e* family.  One candidate per lane; its closure sum
+// comes from the cache (ccache, valid unless an event since marked it stale),
+// else from a lane walk (closure_lane), else -- frontier wider than the lane
+// heap -- from a warp BFS (msps_closure).  Exact branch and bound as in
+// score_stream: every candidate whose closure is known (no evicted neighbour,
+// or a cache hit) is scored in the stream; the score with an EMPTY closure is
+// a lower bound of a stale one's (the closure only adds cost to the
+// numerator), so only stale candidates whose bound is
+// not excluded by the team's best key are walked.  With a stack (st.e: CTA
+// cells with global state, the whole-GPU engine) the stale candidates are
+// stacked during the stream; without one (state in shared memory) pass 2
+// re-scans the pool.  sbest: as in score_stream (null: one-warp team).
 template <bool SM, bool BM>
 __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u32 wrank, u32 wsize,
-                                             volatile u32 *msps_tail, u64 &bytes, u64 &evals, Cand &best, u32 &bk) {
+                                             volatile u32 *msps_tail, u64 &bytes, u64 &evals, Cand &best, u32 &bk,
+                                             const SlowStack &st, u32 *sbest) {
   // CTA: one BFS slot per scoring warp; whole GPU (msps_lock): every warp walks
   // lanes, and the rare BFS fallback locks one of the bounded slots
   const bool locked = g.L.msps_lock != 0;
   const u32 nw = locked || wsize < g.L.msps_warps ? wsize : g.L.msps_warps;
-  if (wrank >= nw) return;
+  const bool active = wrank < nw;
   const u32 lane = threadIdx.x & 31;
-  {
-    // one candidate per lane (closure_lane: ancestors; the e* family also
-    // descendants); a lane whose frontier outgrows its heap hands the candidate
-    // to the whole warp (msps_closure)
-    const u32 FULL = 0xffffffffu, n = BM ? cmd.n_ids : cmd.pool_size;
-    const bool down = cmd.heur != H_MSPS;
-    const bool use_cc = g.L.ccache && cmd.n_ev != NONE;
-    auto finish = [&](u32 t, const uint4 &sr, u64 sum) {
-      Cand c;
-      c.id = t;
-      if (cmd.heur == H_DTR_FULL) {            // (c(S) + sum_{e*(S)} c) / (size(S) * stale(S))
-        stale_score((u64)sr.y + sum, sr.x, sr.z, cmd.clock, c.num, c.den);
-      } else if (is_abl(cmd.heur)) {           // h'(s, m, e*)
-        abl_finish((u64)sr.y + sum, sr.x, sr.z, cmd, c);
-      } else {                                 // MSPS and h_e* (P:1835-1837): (c0 + sum) / m
-        c.num = (u64)sr.y + sum;
-        c.den = sr.x;
+  const u32 FULL = 0xffffffffu, n = BM ? cmd.n_ids : cmd.pool_size;
+  const bool down = cmd.heur != H_MSPS;
+  const bool use_cc = g.L.ccache && cmd.n_ev != NONE;
+  auto make = [&](u32 t, const uint4 &sr, u64 sum) {
+    Cand c;
+    c.id = t;
+    if (cmd.heur == H_DTR_FULL) {            // (c(S) + sum_{e*(S)} c) / (size(S) * stale(S))
+      stale_score((u64)sr.y + sum, sr.x, sr.z, cmd.clock, c.num, c.den);
+    } else if (is_abl(cmd.heur)) {           // h'(s, m, e*)
+      abl_finish((u64)sr.y + sum, sr.x, sr.z, cmd, c);
+    } else {                                 // MSPS and h_e* (P:1835-1837): (c0 + sum) / m
+      c.num = (u64)sr.y + sum;
+      c.den = sr.x;
+    }
+    return c;
+  };
+  constexpr u32 U = SM ? 1 : 4;            // global-memory state: four chunks' loads in flight per lane
+  // U chunks of candidates: ids, score records and (nev > 0) cached closure halves
+  auto fetch = [&](u32 base, u32 *tj, uint4 *srj, uint2 *ccj) {
+#pragma unroll
+    for (u32 j = 0; j < U; j++) {
+      const u32 i = base + j * nw * 32 + lane;
+      tj[j] = NONE;
+      if (i < n) {
+        if constexpr (BM) { if (g.in_pool(i)) tj[j] = i; }
+        else tj[j] = g.pool_ids(i);
       }
-      bytes += 16;
-      evals++;
-      cand_take(best, bk, c);
-    };
-    constexpr u32 U = SM ? 1 : 4;            // global-memory state: four chunks' loads in flight per lane
+    }
+#pragma unroll
+    for (u32 j = 0; j < U; j++) srj[j] = tj[j] != NONE ? g.srec(tj[j]) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (u32 j = 0; j < U; j++) ccj[j] = use_cc && srj[j].w ? g.ccache(tj[j]) : make_uint2(0, 0);
+  };
+  auto known = [&](const uint4 &sr, const uint2 &cc) { return !sr.w || (cc.x && (!down || cc.y)); };
+  // walk the stale closure of one candidate per lane (NONE: idle lane); warp-collective
+  auto resolve = [&](u32 t) {
+    uint4 sr = make_uint4(0, 0, 0, 0);
+    uint2 cc = make_uint2(0, 0);
+    if (t != NONE) { sr = g.srec(t); if (use_cc) cc = g.ccache(t); }
+    bool ok = true;
+    if (t != NONE) {
+      u64 up = cc.x ? cc.x - 1u : 0, dn = cc.y ? cc.y - 1u : 0, b = 0;
+      const bool wu = !cc.x, wd = down && !cc.y;
+      PROF_ADD(17, 1);
+      const uint4 ar = g.arec(t);
+      ok = (!wu || closure_lane<SM, false>(g, t, ar, up, b)) && (!wd || closure_lane<SM, true>(g, t, ar, dn, b));
+      if (ok) {
+        bytes += b;
+        if (use_cc) g.ccache(t) = make_uint2((u32)up + 1u, down ? (u32)dn + 1u : 0u);
+        cand_take(best, bk, make(t, sr, up + dn));
+      }
+      bytes += 16;                           // adjacency record
+    }
+    u32 ov = __ballot_sync(FULL, t != NONE && !ok);
+    while (ov) {
+      const u32 l = __ffs(ov) - 1;
+      ov &= ov - 1;
+      const u32 tt = __shfl_sync(FULL, t, l);
+      u32 slot = wrank;
+      if (locked) {                            // acquire a free slot (its holder always finishes)
+        if (lane == 0) {
+          u32 k = wrank % g.L.msps_warps;
+          while (atomicCAS(&g.m.w(g.L.msps_lock + k), 0u, 1u) != 0u) k = k + 1 == g.L.msps_warps ? 0 : k + 1;
+          __threadfence();
+          slot = k;
+        }
+        slot = __shfl_sync(FULL, slot, 0);
+      }
+      u64 u2 = 0;
+      if (lane == 0) PROF_ADD(18, 1);
+      const u64 s2 = msps_closure(g, g.arec(tt), slot, msps_tail + (threadIdx.x >> 5), bytes, tt, down, &u2);
+      if (locked && lane == 0) { __threadfence(); atomicExch(&g.m.w(g.L.msps_lock + slot), 0u); }
+      if (lane == l) {
+        if (use_cc) g.ccache(tt) = make_uint2((u32)u2 + 1u, down ? (u32)(s2 - u2) + 1u : 0u);
+        cand_take(best, bk, make(tt, sr, s2));
+      }
+    }
+  };
+  u32 nq = 0;                                  // stack depth (warp-uniform)
+  // ---- the stream: candidates whose closure is known; stale ones stacked (or left for the re-scan)
+  if (active) {
     for (u32 base = wrank * 32; base < n; base += U * nw * 32) {
       u32 tj[U];
       uint4 srj[U];
       uint2 ccj[U];
+      fetch(base, tj, srj, ccj);
+      if (st.e) {
+#pragma unroll
+        for (u32 j = 0; j < U; j++) {
+          const bool stale = tj[j] != NONE && !known(srj[j], ccj[j]);
+          const u32 m = __ballot_sync(FULL, stale);
+          if (stale) st.e[nq + __popc(m & ((1u << lane) - 1))] = make_uint2(tj[j], cand_key(make(tj[j], srj[j], 0)));
+          nq += __popc(m);
+        }
+      }
 #pragma unroll
       for (u32 j = 0; j < U; j++) {
-        const u32 i = base + j * nw * 32 + lane;
-        tj[j] = NONE;
-        if (i < n) {
-          if constexpr (BM) { if (g.in_pool(i)) tj[j] = i; }
-          else tj[j] = g.pool_ids(i);
-        }
+        if (tj[j] == NONE) continue;
+        evals++;
+        bytes += 16;                           // score record
+        if (srj[j].w) bytes += use_cc ? 8 : 0; // cached halves
+        if (!known(srj[j], ccj[j])) continue;  // stale
+        PROF_ADD(16, srj[j].w ? 1 : 0);
+        const u64 sum = srj[j].w ? (u64)(ccj[j].x - 1u) + (down ? (u64)(ccj[j].y - 1u) : 0ull) : 0ull;
+        cand_take(best, bk, make(tj[j], srj[j], sum));
       }
+      if (st.e) {
+        __syncwarp();
+        if (nq + 32 * U > st.cap) stack_drain(st, nq, st.cap / 2, team_bound(bk, sbest), resolve);
+      }
+    }
+  }
+  // ---- the team's best key, then the stale closures it does not exclude
+  u32 cur = team_bound(bk, sbest);
+  if (sbest) {
+    __syncthreads();
+    cur = team_bound(bk, sbest);
+  }
+  if (!active) return;
+  if (st.e) {
+    stack_drain(st, nq, 0, cur, resolve);
+    return;
+  }
+  for (u32 base = wrank * 32; base < n; base += U * nw * 32) {   // re-scan (state in shared memory)
+    u32 tj[U];
+    uint4 srj[U];
+    uint2 ccj[U];
+    fetch(base, tj, srj, ccj);
 #pragma unroll
-      for (u32 j = 0; j < U; j++) srj[j] = tj[j] != NONE ? g.srec(tj[j]) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (u32 j = 0; j < U; j++) ccj[j] = use_cc && srj[j].w ? g.ccache(tj[j]) : make_uint2(0, 0);
-#pragma unroll
-      for (u32 j = 0; j < U; j++) {
-      const u32 t = tj[j];
-      const uint4 sr = srj[j];
-      bool ok = true;
-      u64 sum = 0;
-      if (t != NONE && sr.w) {                 // nev = 0: no evicted neighbour, the closure is empty
-        // cached halves {up+1, down+1} (0 = stale), else walked and stored
-        const uint2 cc = ccj[j];
-        u64 up = cc.x ? cc.x - 1u : 0, dn = cc.y ? cc.y - 1u : 0, b = 0;
-        const bool wu = !cc.x, wd = down && !cc.y;
-        if (use_cc) bytes += 8;
-        PROF_ADD(16, (wu || wd) ? 0 : 1);
-        PROF_ADD(17, (wu || wd) ? 1 : 0);
-        if (wu || wd) {
-          const uint4 ar = g.arec(t);
-          ok = (!wu || closure_lane<SM, false>(g, t, ar, up, b)) && (!wd || closure_lane<SM, true>(g, t, ar, dn, b));
-          if (ok) {
-            bytes += b;
-            if (use_cc) g.ccache(t) = make_uint2((u32)up + 1u, down ? (u32)dn + 1u : 0u);
-          }
-          bytes += 16;                         // adjacency record
-        }
-        if (ok) sum = up + dn;
+    for (u32 j = 0; j < U; j++) {
+      u32 t = tj[j];
+      if (t != NONE && known(srj[j], ccj[j])) t = NONE;
+      if (t != NONE && cur != KEY_NONE) {
+        const u32 lb = cand_key(make(t, srj[j], 0));
+        const u32 c2 = bk < cur ? bk : cur;
+        if (lb > c2 + KEY_MARGIN) t = NONE;    // excluded: lb > an exact score already found
       }
-      if (t != NONE && ok) finish(t, sr, sum);
-      u32 ov = __ballot_sync(FULL, t != NONE && !ok);
-      while (ov) {
-        const u32 l = __ffs(ov) - 1;
-        ov &= ov - 1;
-        const u32 tt = __shfl_sync(FULL, t, l);
-        u32 slot = wrank;
-        if (locked) {                            // acquire a free slot (its holder always finishes)
-          if (lane == 0) {
-            u32 k = wrank % g.L.msps_warps;
-            while (atomicCAS(&g.m.w(g.L.msps_lock + k), 0u, 1u) != 0u) k = k + 1 == g.L.msps_warps ? 0 : k + 1;
-            __threadfence();
-            slot = k;
-          }
-          slot = __shfl_sync(FULL, slot, 0);
-        }
-        u64 u2 = 0;
-        if (lane == 0) PROF_ADD(18, 1);
-        const u64 s2 = msps_closure(g, g.arec(tt), slot, msps_tail + (threadIdx.x >> 5), bytes, tt, down, &u2);
-        if (locked && lane == 0) { __threadfence(); atomicExch(&g.m.w(g.L.msps_lock + slot), 0u); }
-        if (lane == l) {
-          if (use_cc) g.ccache(tt) = make_uint2((u32)u2 + 1u, down ? (u32)(s2 - u2) + 1u : 0u);
-          finish(tt, sr, s2);
-        }
-      }
-      }
+      resolve(t);
     }
   }
 }
@@ -896,28 +1014,29 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
 // WIDE: global-memory team (four candidates in flight per thread, else two).
 template <bool SM, bool BM, bool WIDE = false, bool CL = true>
 __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, u32 wrank, u32 wsize,
-                           volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk, u32 *wq = nullptr) {
+                           volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk,
+                           const SlowStack &st = SlowStack{nullptr, 0}, u32 *sbest = nullptr) {
   Cand best = cand_none();
   bk = KEY_NONE;
   if (BM && rank == 0) bytes += (cmd.n_ids + 7) / 8;     // the pool bitmap
   if constexpr (CL) {   // CL = false: a kernel built for batches without closure heuristics (dtr.cu)
     if (uses_closure(cmd.heur)) {
-      team_closure<SM, BM>(g, cmd, wrank, wsize, msps_tail, bytes, evals, best, bk);
+      team_closure<SM, BM>(g, cmd, wrank, wsize, msps_tail, bytes, evals, best, bk, st, sbest);
       return best;
     }
   }
   constexpr u32 K = WIDE ? 4 : 2;
   if constexpr (!SM && BM) {
     switch (cmd.heur) {
-      case H_DTR: score_stream<false, true, H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
-      case H_DTR_EQ: score_stream<false, true, H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
-      case H_LRU: score_stream<false, true, H_LRU, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
-      case H_SIZE: score_stream<false, true, H_SIZE, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
-      case H_LOCAL: score_stream<false, true, H_LOCAL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
-      case H_RANDOM: score_stream<false, true, H_RANDOM, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best;
+      case H_DTR: score_stream<false, true, H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, st, sbest); return best;
+      case H_DTR_EQ: score_stream<false, true, H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, st, sbest); return best;
+      case H_LRU: score_stream<false, true, H_LRU, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, st, sbest); return best;
+      case H_SIZE: score_stream<false, true, H_SIZE, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, st, sbest); return best;
+      case H_LOCAL: score_stream<false, true, H_LOCAL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, st, sbest); return best;
+      case H_RANDOM: score_stream<false, true, H_RANDOM, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, st, sbest); return best;
       default:
         if (is_abl(cmd.heur) && abl_c(cmd.heur) != ABL_ESTAR) {
-          score_stream<false, true, H_ABL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq);
+          score_stream<false, true, H_ABL, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, st, sbest);
           return best;
         }
         break;
@@ -929,9 +1048,9 @@ __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size,
     return best;
   }
   if constexpr (!SM) {   // state in global memory (CTA engine): the stream pass with its slow stack
-    if (wq) {
-      if (cmd.heur == H_DTR) { score_stream<false, false, H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best; }
-      if (cmd.heur == H_DTR_EQ) { score_stream<false, false, H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, wq); return best; }
+    if (st.e) {
+      if (cmd.heur == H_DTR) { score_stream<false, false, H_DTR, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, st, sbest); return best; }
+      if (cmd.heur == H_DTR_EQ) { score_stream<false, false, H_DTR_EQ, 4>(g, cmd, wrank, wsize, best, bk, bytes, evals, st, sbest); return best; }
     }
   }
   switch (cmd.heur) {

@@ -17,7 +17,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from .binding import (DeviceBatch, RESULT_DTYPE, ENGINE_CTA, ENGINE_GRID, HEURISTICS, GRID_MIN_TENSORS)
+from .binding import (DeviceBatch, RESULT_DTYPE, ENGINE_CTA, ENGINE_GRID, HEURISTICS, GRID_MIN_TENSORS,
+                      cta_class)
 
 # relative per-decision cost of a heuristic's score (MSPS walks closures)
 HEUR_WEIGHT = {0: 3.0, 1: 3.0, 2: 1.0, 3: 1.0, 4: 6.0, 5: 1.5, 6: 1.0, 7: 8.0, 8: 8.0}
@@ -36,7 +37,11 @@ def make_cells(log_views, permilles, heuristics, thrash_kill=16, max_decisions=0
     return cells
 
 
-def est_cost(cell, log_views):
+def est_cost(cell, log_views, costs=None):
+    """Estimated cost of a cell: its MEASURED device time (costs[cell_id], e.g. the
+    wall_ns of a previous run's row) when given, else a static guess."""
+    if costs is not None and cell["cell_id"] in costs:
+        return float(costs[cell["cell_id"]])
     v = log_views[cell["log"]]
     pm = max(int(cell.get("permille", 1000)), 50)
     h = cell["heuristic"]
@@ -44,16 +49,16 @@ def est_cost(cell, log_views):
     return v.n_ops * (1000.0 / pm) * w
 
 
-def shard(cells, log_views, world_size):
-    """Deterministic LPT: sort by estimated cost (desc, then cell id), give each
-    cell to the least-loaded rank (ties -> lowest rank). Returns per-rank lists."""
-    order = sorted(cells, key=lambda c: (-est_cost(c, log_views), c["cell_id"]))
+def shard(cells, log_views, world_size, costs=None):
+    """Deterministic LPT: sort by (estimated or measured) cost (desc, then cell id),
+    give each cell to the least-loaded rank (ties -> lowest rank). Returns per-rank lists."""
+    order = sorted(cells, key=lambda c: (-est_cost(c, log_views, costs), c["cell_id"]))
     load = [0.0] * world_size
     out = [[] for _ in range(world_size)]
     for c in order:
         r = min(range(world_size), key=lambda k: (load[k], k))
         out[r].append(c)
-        load[r] += est_cost(c, log_views)
+        load[r] += est_cost(c, log_views, costs)
     for r in range(world_size):
         out[r].sort(key=lambda c: c["cell_id"])
     return out
@@ -67,13 +72,24 @@ def engine_groups(cells, log_views):
 
 
 class RankSweep:
-    """The device side of one rank: its cells as (up to) two resident batches."""
+    """The device side of one rank: its cells as (up to) two resident batches.
 
-    def __init__(self, logs, log_views, cells, device=None):
+    CTA cells are grouped by shared-memory class (one launch each, the classes
+    run concurrently) and, inside a class, ordered LONGEST FIRST by cost --
+    measured device times when `costs` is given (sweep rows' wall_ns), else
+    the static estimate: the hardware dispatches a launch's CTAs in order as
+    SMs free up, so this is a longest-first work queue and the long cells
+    never start in the last wave."""
+
+    def __init__(self, logs, log_views, cells, device=None, costs=None):
         self.cells = cells
         cta, grid = engine_groups(cells, log_views)
-        # order CTA cells by log so shared-memory classes form few launches
-        cta.sort(key=lambda c: (log_views[c["log"]].n, c["log"], c["cell_id"]))
+
+        def key(c):
+            v = log_views[c["log"]]
+            return (cta_class(v.n, v.n_edges, c["heuristic"]), -est_cost(c, log_views, costs), c["cell_id"])
+        cta.sort(key=key)
+        grid.sort(key=lambda c: (-est_cost(c, log_views, costs), c["cell_id"]))
         self.order = cta + grid
         self.batches = []
         for group, eng in ((cta, ENGINE_CTA), (grid, ENGINE_GRID)):

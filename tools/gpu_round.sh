@@ -1,5 +1,5 @@
 # One GPU session for the round's evidence: smoke, tests, bench, launch list,
-# ncu --set full of the top kernels (run under gpurun).  usage: bash scripts/gpu_round.sh TAG
+# ncu --set full of the top kernels (run under gpurun).  usage: bash tools/gpu_round.sh TAG
 set -x
 TAG=${1:-s2}
 O=gpurun_out/$TAG
@@ -12,7 +12,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     python bench.py --steps 2 --warmup 3 --no-extra --no-large-pool --no-cpu > $O/bench_ncu.log 2>&1; echo ncu_launch=$?
 for n in 1000000 4000000; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:pool_argmin -s 2 -c 1 -o $O/pa_full_$n \
-      python scripts/pool_argmin_one.py $n 0 > $O/ncu_pa_$n.log 2>&1; echo ncu_pa_$n=$?
+      python tools/pool_argmin_one.py $n 0 > $O/ncu_pa_$n.log 2>&1; echo ncu_pa_$n=$?
   ncu -i $O/pa_full_$n.ncu-rep --page raw --csv > $O/pa_raw_$n.csv 2>/dev/null
   ncu -i $O/pa_full_$n.ncu-rep --page details --csv > $O/pa_details_$n.csv 2>/dev/null
   ncu -i $O/pa_full_$n.ncu-rep --page source --csv --print-source sass > $O/pa_source_sass_$n.csv 2>/dev/null

@@ -10,5 +10,5 @@ for k in ('roofline_large_pool','roofline_large_pool_4e6'): print(k, round(d[k][
 print('value', d['value'], d['ms_per_step'])"
 python paper_2006_09616_b200/_build.py --profile > /dev/null 2>&1; echo profbuild=$?
 for c in "transformer msps 317 3000" "densenet100 msps 317 3000" "lstm msps 317 3000" "treelstm msps 317 3000" "lstm dtr_eq 317 20000" "lstm dtr 100 20000" "treelstm dtr 100 20000" "resnet32 size 286 0"; do
-  timeout 300 python scripts/probe_prof_c5.py $c 2>&1 | tail -5
+  timeout 300 python tools/probe_prof_c5.py $c 2>&1 | tail -5
 done > gpurun_out/s5/prof.log; cat gpurun_out/s5/prof.log

@@ -1,5 +1,5 @@
 """Phase profile (clock64 build, libdtr_prof.so) of single config-5 cells:
-python scripts/probe_prof_c5.py MODEL HEUR PERMILLE [MAX_DECISIONS]"""
+python tools/probe_prof_c5.py MODEL HEUR PERMILLE [MAX_DECISIONS]"""
 import ctypes as C, os, sys, time
 os.environ["DTR_LIB"] = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                      "paper_2006_09616_b200", "libdtr_prof.so")
