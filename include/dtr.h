@@ -294,6 +294,16 @@ int dtr_debug_set_budget(dtr_runtime *rt, uint64_t budget);
 int dtr_debug_scores(dtr_runtime *rt, uint64_t *num, uint64_t *den, uint32_t *ids, uint64_t cap,
                      uint64_t *n_out);
 
+/* Residency of every tensor created so far (the state of memory visualised in
+ * PAPER.md App. A, Fig. "trace"): out[t] = DTR_T_UNCOMPUTED (0:
+ * MAKE started, first computation not finished), DTR_T_RESIDENT (1: t.m = T),
+ * DTR_T_EVICTED (2: t.m = F after a computation) or DTR_T_BANISHED (3: removed
+ * from the graph by V1 banishing).  out: host, cap bytes; *n_out =
+ * tensors created (only min(cap, n) are written).  Returns DTR_OK /
+ * DTR_E_INVAL / DTR_E_CUDA; no state change. */
+enum { DTR_T_UNCOMPUTED = 0, DTR_T_RESIDENT = 1, DTR_T_EVICTED = 2, DTR_T_BANISHED = 3 };
+int dtr_debug_state(dtr_runtime *rt, uint8_t *out, uint64_t cap, uint64_t *n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,7 +54,7 @@ assert ADV_DTYPE.itemsize == 40
 EXPORTS = ["dtr_strerror", "dtr_last_cuda_error", "dtr_version", "dtr_batch_workspace_bytes", "dtr_cta_class",
            "dtr_replay_batch", "dtr_replay_batch_host", "dtr_create", "dtr_destroy", "dtr_compute", "dtr_get",
            "dtr_release", "dtr_rematerialize", "dtr_ensure", "dtr_stats", "dtr_trace", "dtr_debug_evict",
-           "dtr_debug_set_budget", "dtr_debug_scores", "dtr_pool_argmin", "dtr_adversary_workspace_bytes",
+           "dtr_debug_set_budget", "dtr_debug_scores", "dtr_debug_state", "dtr_pool_argmin", "dtr_adversary_workspace_bytes",
            "dtr_adversary_batch"]
 
 
@@ -112,6 +112,8 @@ def _load():
     L.dtr_debug_set_budget.argtypes = [P, u64]
     L.dtr_debug_scores.restype = i32
     L.dtr_debug_scores.argtypes = [P, P, P, P, u64, C.POINTER(u64)]
+    L.dtr_debug_state.restype = i32
+    L.dtr_debug_state.argtypes = [P, P, u64, C.POINTER(u64)]
     return L
 
 
@@ -392,6 +394,14 @@ class Runtime:
         _check(lib.dtr_debug_scores(self.h, _np_ptr(num), _np_ptr(den), _np_ptr(ids), cap, C.byref(n)),
                "dtr_debug_scores")
         return {int(ids[i]): (int(num[i]), int(den[i])) for i in range(n.value)}
+
+    def state(self):
+        """Residency of every created tensor: 0 uncomputed, 1 resident, 2 evicted, 3 banished."""
+        cap = self.cap_tensors + 1
+        out = np.zeros(cap, np.uint8)
+        n = C.c_uint64(0)
+        _check(lib.dtr_debug_state(self.h, _np_ptr(out), cap, C.byref(n)), "dtr_debug_state")
+        return out[: min(n.value, cap)].copy()
 
     def stats(self):
         r = np.zeros(1, dtype=RESULT_DTYPE)

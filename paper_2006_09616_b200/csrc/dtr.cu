@@ -484,6 +484,24 @@ int dtr_debug_scores(dtr_runtime *rt, uint64_t *num, uint64_t *den, uint32_t *id
   return DTR_OK;
 }
 
+int dtr_debug_state(dtr_runtime *rt, uint8_t *out, uint64_t cap, uint64_t *n_out) {
+  if (!rt || !n_out || (cap && !out)) return DTR_E_INVAL;
+  int rc = rt_sync_scalars(rt);
+  if (rc) return rc;
+  const u64 n = rt->hs.n_alloc;
+  *n_out = n;
+  const u64 m = std::min<u64>(n, cap);
+  if (!m) return DTR_OK;
+  std::vector<u32> st(m);
+  CK(cudaMemcpyAsync(st.data(), rt->d_ws + rt->L.state, 4 * m, cudaMemcpyDeviceToHost, rt->st));
+  CK(cudaStreamSynchronize(rt->st));
+  for (u64 t = 0; t < m; t++) {   // state word: bit31 material, bit30 computed once, bit29 banished
+    const u32 w = st[t];
+    out[t] = (w & B_BIT) ? DTR_T_BANISHED : (w & M_BIT) ? DTR_T_RESIDENT : (w & O_BIT) ? DTR_T_EVICTED : DTR_T_UNCOMPUTED;
+  }
+  return DTR_OK;
+}
+
 int dtr_stats(dtr_runtime *rt, dtr_result *out) {
   if (!rt || !out) return DTR_E_INVAL;
   int rc = rt_sync_scalars(rt);

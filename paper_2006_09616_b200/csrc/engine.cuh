@@ -91,7 +91,7 @@ enum { OP_MAKE = 1, OP_GET = 2, OP_RELEASE = 3, OP_REMAT = 4, OP_ENSURE = 5, OP_
 // rematerialization, V1 banish of an evicted tensor); before the next score
 // pass the team walks from each queued tensor and marks stale the caches it may
 // have changed.  More than EVQ_CAP events between two decisions = all stale.
-constexpr u32 EVQ_CAP = 64;
+constexpr u32 EVQ_CAP = 1024;
 enum { DEALLOC_V2 = 0, DEALLOC_V1 = 1, DEALLOC_EAGER = 2, DEALLOC_IGNORE = 3 };
 enum { ST_OK = 0, ST_INVAL = 1, ST_PRECOND = 2, ST_OOM = 3, ST_THRASH = 4, ST_CAPACITY = 5,
        ST_STATE = 6, ST_DECISION_CAP = 8 };

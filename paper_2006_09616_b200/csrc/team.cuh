@@ -625,6 +625,7 @@ __device__ __forceinline__ void stack_drain(const SlowStack &st, u32 &nq, u32 ke
     out += __popc(m);
     __syncwarp();
   }
+  if (lane == 0) { PROF_ADD(22, nq); PROF_ADD(23, out); }
   nq = out;
   while (nq > keep) {
     u32 take = nq - keep;
@@ -903,6 +904,9 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
   auto known = [&](const uint4 &sr, const uint2 &cc) { return !sr.w || (cc.x && (!down || cc.y)); };
   // walk the stale closure of one candidate per lane (NONE: idle lane); warp-collective
   auto resolve = [&](u32 t) {
+#ifdef DTR_PROFILE
+    { const u32 m = __ballot_sync(FULL, t != NONE); if (lane == 0) PROF_ADD(17, __popc(m)); }
+#endif
     uint4 sr = make_uint4(0, 0, 0, 0);
     uint2 cc = make_uint2(0, 0);
     if (t != NONE) { sr = g.srec(t); if (use_cc) cc = g.ccache(t); }
@@ -910,7 +914,6 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
     if (t != NONE) {
       u64 up = cc.x ? cc.x - 1u : 0, dn = cc.y ? cc.y - 1u : 0, b = 0;
       const bool wu = !cc.x, wd = down && !cc.y;
-      PROF_ADD(17, 1);
       const uint4 ar = g.arec(t);
       ok = (!wu || closure_lane<SM, false>(g, t, ar, up, b)) && (!wd || closure_lane<SM, true>(g, t, ar, dn, b));
       if (ok) {
@@ -969,10 +972,15 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
         bytes += 16;                           // score record
         if (srj[j].w) bytes += use_cc ? 8 : 0; // cached halves
         if (!known(srj[j], ccj[j])) continue;  // stale
-        PROF_ADD(16, srj[j].w ? 1 : 0);
         const u64 sum = srj[j].w ? (u64)(ccj[j].x - 1u) + (down ? (u64)(ccj[j].y - 1u) : 0ull) : 0ull;
         cand_take(best, bk, make(tj[j], srj[j], sum));
       }
+#ifdef DTR_PROFILE
+      for (u32 j = 0; j < U; j++) {
+        const u32 m = __ballot_sync(FULL, tj[j] != NONE && srj[j].w && known(srj[j], ccj[j]));
+        if (lane == 0) PROF_ADD(16, __popc(m));
+      }
+#endif
       if (st.e) {
         __syncwarp();
         if (nq + 32 * U > st.cap) stack_drain(st, nq, st.cap / 2, team_bound(bk, sbest), resolve);

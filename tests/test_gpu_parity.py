@@ -563,3 +563,29 @@ def _msps_wide(P, O, width):
     tr = o.trace()
     assert int(tr[0]["id"]) == y and int(tr[0]["num"]) == 1 + 50 * width   # the exact closure sum decided it
     assert g.trace().tobytes() == tr.tobytes()
+
+
+def test_percall_state_residency_vs_oracle(P, oracle_mod):
+    """dtr_debug_state (the App. A residency trace) equals the oracle's
+    per-tensor flags after every record: the linear net, N = 64, B = 2 sqrt(N),
+    h_e* with V1 banishing (the Theorem 1 setting) and h_DTR with V2."""
+    from dtr_inputs.logfmt import OP_GET, OP_MAKE, OP_RELEASE, OP_SHIFT
+    O = oracle_mod
+    N = 64
+    v = LogView(models.linear(N))
+    for h, dealloc in (("estar", "v1"), ("dtr", "v2")):
+        rt = P.Runtime(P.HEURISTICS[h], budget=16, dealloc=P.DEALLOC[dealloc], cap_tensors=4 * N, cap_edges=8 * N)
+        ref = O.Runtime(O.HEURISTICS[h], budget=16, dealloc=O.DEALLOC[dealloc])
+        for k, w in enumerate(v.ops):
+            op, t = int(w) >> OP_SHIFT, int(w) & ((1 << OP_SHIFT) - 1)
+            if op == OP_MAKE:
+                a, b = rt.compute(int(v.mem[t]), int(v.cost[t]), v.parents(t)), ref.compute(int(v.mem[t]), int(v.cost[t]), v.parents(t))
+                assert a == b
+            elif op == OP_GET:
+                assert rt.get(t) == ref.get(t) == 0
+            elif op == OP_RELEASE:
+                assert rt.release(t) == ref.release(t) == 0
+            fl = ref.tensors()[0]
+            want = [3 if f & 8 else 1 if f & 1 else 2 if f & 2 else 0 for f in fl]
+            assert rt.state().tolist() == want, (h, k)
+        rt.close()
