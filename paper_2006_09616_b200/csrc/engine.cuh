@@ -112,6 +112,7 @@ struct Lay {
   u32 node_of, uf, uf_size, uf_cap;                    // h_DTR_eq (uf rec: {cost lo, cost hi, maxla, parent})
   u32 msps_bm, msps_q, msps_words, msps_warps;         // closure BFS scratch: msps_warps slots
   u32 msps_lock;                                       // grid: slot locks (0 = CTA: slot = warp)
+  u32 msps_d;                                          // per slot: candidate masks of the multi-candidate walk (0 = none)
   u32 e_next, e_child;                                 // linked children (per-call)
   u32 ccache, evq;                                     // closure cache {up+1, down+1} per tensor (0 = stale)
                                                        // + the leader's event queue (batch engines only)
@@ -122,8 +123,10 @@ struct Lay {
 // layout does not fit 32-bit word offsets (the caller reports DTR_E_CAPACITY).
 // msps_warps: closure-BFS scratch slots (one per scoring warp on a CTA; on the
 // whole-GPU engine a bounded number of slots that warps lock, grid_closure_slots).
+// multi: closure heuristics get the per-slot mask arrays of the multi-candidate
+// walk (closure_multi; global-state cells and the whole-GPU engine only).
 __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 linked, u32 msps_warps,
-                                            u32 grid = 0) {
+                                            u32 grid = 0, u32 multi = 0) {
   u64 o = 0;
   auto take = [&](u64 words) -> u32 { u64 p = o; o = (o + words + 3) & ~3ull; return (u32)p; };
   const u64 n1 = (u64)n + 1, e1 = (u64)E + 1;
@@ -146,7 +149,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
   L.mem_next = L.comp = L.comp_head = L.bfs_q = L.stamp = 0;
   L.mem_prev = L.comp_free = 0;
   L.node_of = L.uf = L.uf_size = L.uf_cap = 0;
-  L.msps_bm = L.msps_q = L.msps_words = L.msps_warps = L.msps_lock = 0;
+  L.msps_bm = L.msps_q = L.msps_words = L.msps_warps = L.msps_lock = L.msps_d = 0;
   L.e_next = L.e_child = 0;
   L.ccache = L.evq = 0;
   if (heur == H_DTR) {
@@ -168,6 +171,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
     L.msps_bm = take((u64)L.msps_words * msps_warps);
     L.msps_q = take(n1 * msps_warps);
     if (grid) L.msps_lock = take(msps_warps);
+    if (multi && !linked) L.msps_d = take(n1 * msps_warps);
     if (!linked) {                                     // cached closure sums
       L.ccache = take(2 * n1);
       L.evq = take(EVQ_CAP);
@@ -186,7 +190,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
 // (256 MiB) in total; the lane-parallel walk needs no scratch and the BFS is
 // only the fallback for frontiers wider than the lane heap.
 __host__ __device__ inline u32 grid_closure_slots(u32 n) {
-  const u64 per = (u64)n + 1 + ((u64)n + 32) / 32;
+  const u64 per = 2 * ((u64)n + 1) + ((u64)n + 32) / 32;
   u64 k = (64ull << 20) / per;
   return k < 1 ? 1u : (k > 1024 ? 1024u : (u32)k);
 }

@@ -42,7 +42,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Sim<SM> g;
   g.m.gbase = gbase;
-  make_layout(g.L, logw[2], logw[3], cell.heuristic, 0, CTA_THREADS / 32);
+  make_layout(g.L, logw[2], logw[3], cell.heuristic, 0, CTA_THREADS / 32, 0, SM ? 0 : 1);
   PROF_T(ti0);
   const u64 t_start = gtimer();
   init_sim(g, logw, tid, blockDim.x, true, sh.scan, CtaSync());
@@ -50,8 +50,9 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   if (tid == 0) PROF_ADD(6, ti1 - ti0);
   u64 bytes = 0, evals = 0;
   // global-memory state: the dynamic shared memory holds the per-warp slow stacks (score_stream)
-  const SlowStack wq = SM ? SlowStack{nullptr, 0}
-                          : SlowStack{reinterpret_cast<uint2 *>(g_smem) + warp * CTA_WQ_PAIRS, CTA_WQ_PAIRS};
+  const SlowStack wq = SM ? SlowStack{nullptr, 0, nullptr}
+                          : SlowStack{reinterpret_cast<uint2 *>(g_smem) + warp * CTA_WQ_PAIRS, CTA_WQ_PAIRS,
+                                      reinterpret_cast<u64 *>(g_smem + 2 * (CTA_THREADS / 32) * CTA_WQ_PAIRS) + 32 * warp};
   if (warp == 0) {
     Leader<SM, false> L;
     if (lane == 0) leader_init(L, g, logw, cell, trace);
@@ -78,7 +79,9 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
         if (lane == 0) { res = intkey_cand(g, c, k); have = true; PROF_ADD(1, t3 - t2); PROF_ADD(3, 1); }
         continue;
       }
-      if (c.kind == CMD_ARGMIN && c.pool_size <= WARP_TEAM_MAX) {
+      // closure heuristics on global state: always the whole CTA (deep closure walks
+      // dominate there, and eight warps drain their stacks concurrently)
+      if (c.kind == CMD_ARGMIN && c.pool_size <= WARP_TEAM_MAX && (SM || !CL || !uses_closure(c.heur))) {
         PROF_T(t2);
         u32 bk;
         Cand best = team_score<SM, false, false, CL>(g, c, lane, 32, 0, 1, sh.msps_tail, bytes, evals, bk, wq);

@@ -13,6 +13,7 @@ struct __align__(16) GridShared {
   ScanSmem scan;
   u32 msps_tail[GRID_THREADS / 32];
   uint2 wq[GRID_THREADS / 32][GRID_WQ_PAIRS];   // per-warp stacks of deferred candidates
+  u64 msum[GRID_THREADS / 32][32];                // per-warp sums of the multi-candidate closure walk
   u32 best;                           // the block's best pass-1 key (score_stream pruning)
 };
 
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
     u32 bk;
     PROF_T(c0);
     Cand best = team_score<false, true, true>(g, sh.cmd, rank, size, wrank, wsize, sh.msps_tail, bytes, evals, bk,
-                                              SlowStack{sh.wq[tid >> 5], GRID_WQ_PAIRS}, &sh.best);
+                                              SlowStack{sh.wq[tid >> 5], GRID_WQ_PAIRS, sh.msum[tid >> 5]}, &sh.best);
     PROF_T(c1);
     const bool ik = int_key_heur(sh.cmd.heur);
     best = block_argmin(best, bk, sh.red, ik);
@@ -139,9 +140,13 @@ struct __align__(16) PaShared {
   RedSmem red;
   u32 msps_tail[PA_THREADS / 32];
   uint2 wq[PA_THREADS / 32][GRID_WQ_PAIRS];
+  u64 msum[PA_THREADS / 32][32];
   u32 last, best;
 };
 
+// CL = false: the instantiation without the K5 closure pass (the hot h_DTR /
+// h_DTR_eq pass then needs no spills under the 64-register bound)
+template <bool CL>
 __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *logw, u32 heur, char *ws,
                                                                     u64 *out /* num, den, id, bytes, evals */) {
   __shared__ PaShared sh;
@@ -161,8 +166,9 @@ __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *l
   u32 bk;
   if (tid == 0) sh.best = KEY_NONE;
   __syncthreads();
-  Cand best = team_score<false, true, true>(g, cmd, rank, size, rank >> 5, size >> 5, sh.msps_tail, bytes, evals, bk,
-                                            SlowStack{sh.wq[tid >> 5], GRID_WQ_PAIRS}, &sh.best);
+  Cand best = team_score<false, true, true, CL>(g, cmd, rank, size, rank >> 5, size >> 5, sh.msps_tail, bytes, evals,
+                                                bk, SlowStack{sh.wq[tid >> 5], GRID_WQ_PAIRS, sh.msum[tid >> 5]},
+                                                &sh.best);
   const bool ik = int_key_heur(heur);
   best = block_argmin(best, bk, sh.red, ik);
   block_sum2(bytes, evals, sh.red);
@@ -203,7 +209,7 @@ namespace dtr {
 cudaError_t grid_occupancy(int *grid_per_sm, int *pa_per_sm) {
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(grid_per_sm, grid_engine, GRID_THREADS, 0);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(pa_per_sm, pool_argmin_kernel, PA_THREADS, 0);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(pa_per_sm, pool_argmin_kernel<false>, PA_THREADS, 0);
 }
 
 cudaError_t launch_grid(int blocks, cudaStream_t st, const u32 *words, const dtr_cell *cells, u32 ci, char *ws,
@@ -214,7 +220,8 @@ cudaError_t launch_grid(int blocks, cudaStream_t st, const u32 *words, const dtr
 }
 
 cudaError_t launch_pool_argmin(int blocks, cudaStream_t st, const u32 *logw, u32 heur, char *ws, u64 *out) {
-  pool_argmin_kernel<<<blocks, PA_THREADS, 0, st>>>(logw, heur, ws, out);
+  if (uses_closure(heur)) pool_argmin_kernel<true><<<blocks, PA_THREADS, 0, st>>>(logw, heur, ws, out);
+  else pool_argmin_kernel<false><<<blocks, PA_THREADS, 0, st>>>(logw, heur, ws, out);
   return cudaGetLastError();
 }
 

@@ -42,7 +42,8 @@ using namespace dtr;
 #define WS_PA_DONE 124       /* dtr_pool_argmin: blocks finished (u32; zeroed by the grid engine) */
 #define CTA_SMEM_MAX (225u * 1024u)
 #define CTA_WQ_PAIRS 1024u   /* global-state cells: per-warp stack of deferred candidates (team.cuh SlowStack) */
-#define CTA_WQ_BYTES (CTA_THREADS / 32 * CTA_WQ_PAIRS * 8)   /* = the dynamic shared memory of those launches */
+#define CTA_WQ_BYTES (CTA_THREADS / 32 * (CTA_WQ_PAIRS * 8 + 32 * 8))   /* stacks + multi-walk sums: the dynamic
+                                                                        shared memory of those launches */
 #define GRID_WQ_PAIRS 192u   /* whole-GPU teams: per-warp stack (>= 32 * 4 steps + 32) */  /* + ~1 KB static CtaShared <= 227 KB per block */
 
 // ---------------------------------------------------------------------------
@@ -109,6 +110,10 @@ __device__ void init_sim(const Sim<SM> &g, const u32 *logw, u32 rank, u32 size, 
     for (u32 i = rank; i < words; i += size) g.m.w(g.L.msps_bm + i) = 0;
     if (g.L.msps_lock)
       for (u32 i = rank; i < g.L.msps_warps; i += size) g.m.w(g.L.msps_lock + i) = 0;
+    if (g.L.msps_d) {
+      const u32 dw = (g.L.n + 1) * g.L.msps_warps;
+      for (u32 i = rank; i < dw; i += size) g.m.w(g.L.msps_d + i) = 0;
+    }
   }
   sync();
   for (u32 c = rank; c < n; c += size) {
@@ -211,7 +216,7 @@ __device__ __forceinline__ void leader_init(Leader<SM, BM> &L, const Sim<SM> &g,
 // 0 = the layout does not fit 32-bit word offsets (DTR_E_CAPACITY)
 __host__ __device__ inline bool cell_layout(Lay &L, u32 n, u32 E, u32 heur, u32 engine) {
   const bool grid = engine == DTR_ENGINE_GRID;
-  return make_layout(L, n, E, heur, 0, grid ? grid_closure_slots(n) : CTA_THREADS / 32, grid);
+  return make_layout(L, n, E, heur, 0, grid ? grid_closure_slots(n) : CTA_THREADS / 32, grid, 1);
 }
 __host__ __device__ inline u64 cell_bytes(u32 n, u32 E, u32 heur, u32 engine) {
   Lay L;

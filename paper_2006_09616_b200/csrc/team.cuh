@@ -149,7 +149,9 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &ar, u32 wslot, volati
 // evicted tensors between itself and t, in the current state), and the
 // descendant half of e*(t) only for the non-evicted t reached upwards; those
 // caches (and x's own) are marked stale.  Walks use the current state, so the
-// order of the events does not matter.  Scratch: closure slot `slot`.
+// order of the events does not matter, and all events are walked as ONE
+// multi-source search per direction (overlapping regions once).  Scratch:
+// closure slot `slot`.
 template <bool SM>
 __device__ void closure_events(const Sim<SM> &g, const Cmd &cmd, u32 slot, volatile u32 *tail) {
   if (!g.L.ccache || cmd.n_ev == 0 || cmd.n_ev == NONE) return;
@@ -163,56 +165,123 @@ __device__ void closure_events(const Sim<SM> &g, const Cmd &cmd, u32 slot, volat
   const u32 bm = g.L.msps_bm + slot * g.L.msps_words;
   const u32 q = g.L.msps_q + slot * (g.L.n + 1);
   PROF_T(ce0);
-  for (u32 e = 0; e < cmd.n_ev; e++) {
-    const u32 x = g.m.w(g.L.evq + e);
-    if (lane == 0) { g.ccache(x) = make_uint2(0, 0); *tail = 0; }
-    __syncwarp();
-    // f = 0: ancestor caches (.x) of the tensors below; f = 1: descendant caches (.y) above
-    auto visit = [&](u32 y, u32 f) {
-      if (!is_evicted(g.state(y))) { g.m.w(g.L.ccache + 2 * y + f) = 0; return; }
-      const u32 bit = 1u << (y & 31);
-      if (atomicOr(&g.m.w(bm + (y >> 5)), bit) & bit) return;
-      g.m.w(q + atomicAdd((u32 *)tail, 1u)) = y;
-    };
-    auto kids = [&](u32 y, u32 j0, u32 dj) {
+  // f = 0: ancestor caches (.x) of the tensors below; f = 1: descendant caches (.y) above
+  auto visit = [&](u32 y, u32 f) {
+    if (!is_evicted(g.state(y))) { g.m.w(g.L.ccache + 2 * y + f) = 0; return; }
+    const u32 bit = 1u << (y & 31);
+    if (atomicOr(&g.m.w(bm + (y >> 5)), bit) & bit) return;
+    g.m.w(q + atomicAdd((u32 *)tail, 1u)) = y;
+  };
+  auto step = [&](u32 y, u32 f) {                // the evicted-side neighbours of y in direction f
+    if (f == 0) {
       const uint2 cr = g.crec(y);
-      for (u32 j = j0; j < cr.y; j += dj) visit(g.m.w(g.L.ch + cr.x + j), 0);
-    };
-    auto pars = [&](u32 y, u32 j0, u32 dj) {
+      for (u32 j = 0; j < cr.y; j++) visit(g.m.w(g.L.ch + cr.x + j), 0);
+    } else {
       const uint2 pr = g.prec(y);
-      for (u32 j = j0; j < pr.y; j += dj) visit(g.par(pr.x + j), 1);
-    };
-    u32 head = 0, tl;
-    kids(x, lane, 32);
+      for (u32 j = 0; j < pr.y; j++) visit(g.par(pr.x + j), 1);
+    }
+  };
+  u32 nodes = 0;
+  for (u32 f = 0; f < (down ? 2u : 1u); f++) {
+    if (lane == 0) *tail = 0;
     __syncwarp();
-    tl = *tail;
+    for (u32 e = lane; e < cmd.n_ev; e += 32) {  // every event is a source
+      const u32 x = g.m.w(g.L.evq + e);
+      if (f == 0) g.ccache(x) = make_uint2(0, 0);
+      step(x, f);
+    }
+    __syncwarp();
+    u32 head = 0, tl = *tail;
     __syncwarp();
     while (head < tl) {
-      for (u32 i = head + lane; i < tl; i += 32) kids(g.m.w(q + i), 0, 1);
+      for (u32 i = head + lane; i < tl; i += 32) step(g.m.w(q + i), f);
       __syncwarp();
       head = tl;
       tl = *tail;
       __syncwarp();
     }
-    if (down) {
-      pars(x, lane, 32);
-      __syncwarp();
-      tl = *tail;
-      __syncwarp();
-      while (head < tl) {
-        for (u32 i = head + lane; i < tl; i += 32) pars(g.m.w(q + i), 0, 1);
-        __syncwarp();
-        head = tl;
-        tl = *tail;
-        __syncwarp();
-      }
-    }
-    for (u32 i = lane; i < tl; i += 32) g.m.w(bm + (g.m.w(q + i) >> 5)) = 0;
-    if (lane == 0) PROF_ADD(20, tl);
+    for (u32 i = lane; i < tl; i += 32) g.m.w(bm + (g.m.w(q + i) >> 5)) = 0;   // fresh visited set per direction
     __syncwarp();
+    nodes += tl;
   }
   PROF_T(ce1);
-  if (lane == 0) { PROF_ADD(19, cmd.n_ev); PROF_ADD(21, ce1 - ce0); }
+  if (lane == 0) { PROF_ADD(19, cmd.n_ev); PROF_ADD(20, nodes); PROF_ADD(21, ce1 - ce0); }
+}
+
+// K5, up to 32 candidates at once (one per lane; NONE = idle lane): ONE walk
+// over the union of their closures, each node carrying the 32-bit mask of the
+// candidates whose closure it is in (closure sets overlap heavily on these
+// graphs: every candidate below an evicted trunk shares it).  visit(y, m): y
+// joins the closures of the candidates in m it was not yet in (atomicOr on its
+// mask word); each newly set bit adds c(y) to that candidate's sum, and y is
+// queued to pass the new bits on -- a node is re-queued only when new bits
+// reach it, so it is expanded at most once per arrival wave, never per
+// candidate.  Up: through evicted parents (e_R); down (the e*
+// family): through evicted children.  Scratch: the slot's mask
+// array (zero on entry and exit) and queue; sums: st.msum.  Returns false
+// (warp-uniform) when the queue overflows (the caller walks per lane instead).
+template <bool SM>
+__device__ bool closure_multi(const Sim<SM> &g, u32 t, u32 slot, volatile u32 *tail, u64 *msum, bool down, u64 &up,
+                              u64 &dn, u64 &bytes) {
+  const u32 lane = threadIdx.x & 31;
+  const u32 n1 = g.L.n + 1;
+  const u32 D = g.L.msps_d + slot * n1, q = g.L.msps_q + slot * n1;
+  bool ovf = false;
+  auto walk = [&](bool dn_dir) -> u64 {
+    msum[lane] = 0;
+    if (lane == 0) *tail = 0;
+    __syncwarp();
+    auto visit = [&](u32 y, u32 m) {
+      bytes += 8;                                  // neighbour id + its state word
+      if (!is_evicted(g.state(y))) return;
+      const u32 old = atomicOr(&g.m.w(D + y), m);
+      const u32 nb = m & ~old;
+      if (!nb) return;
+      if (!old) bytes += 16;                       // its score record (first arrival)
+      const u64 c = g.srec(y).y;
+      for (u32 b = nb; b; b &= b - 1) atomicAdd(&msum[__ffs(b) - 1], c);
+      const u32 pos = atomicAdd((u32 *)tail, 1u);
+      if (pos < n1) g.m.w(q + pos) = y;
+    };
+    auto expand = [&](u32 x, u32 m) {
+      if (!dn_dir) {
+        const uint2 pr = g.prec(x);
+        for (u32 j = 0; j < pr.y; j++) visit(g.par(pr.x + j), m);
+      } else {
+        const uint2 cr = g.crec(x);
+        bytes += 8;
+        for (u32 j = 0; j < cr.y; j++) visit(g.m.w(g.L.ch + cr.x + j), m);
+      }
+    };
+    if (t != NONE) expand(t, 1u << lane);
+    __syncwarp();
+    u32 head = 0, tl = *tail;
+    __syncwarp();
+    while (head < tl && tl <= n1) {
+      for (u32 i = head + lane; i < tl; i += 32) {
+        const u32 x = g.m.w(q + i);
+        expand(x, atomicOr(&g.m.w(D + x), 0u));    // the mask as it stands (later bits re-queue x)
+      }
+      __syncwarp();
+      head = tl;
+      tl = *tail;
+      __syncwarp();
+    }
+    if (tl > n1) {                                 // overflow: some marked nodes were not queued
+      ovf = true;
+      for (u32 y = lane; y < g.L.n; y += 32) g.m.w(D + y) = 0;
+    } else {
+      for (u32 i = lane; i < tl; i += 32) g.m.w(D + g.m.w(q + i)) = 0;
+    }
+    __syncwarp();
+    const u64 r = msum[lane];
+    __syncwarp();
+    return r;
+  };
+  up = walk(false);
+  dn = 0;
+  if (down && !ovf) dn = walk(true);
+  return !ovf;
 }
 
 // K5 closures of ONE candidate per lane (lane-parallel).  UP: e_R(t), the
@@ -385,7 +454,8 @@ __device__ __forceinline__ Cand warp_argmin_fast(const Cand &c, u32 k, bool ik =
 // with la(t).  Used per lane by the whole-GPU team's phase 2 and by score_h.
 constexpr u32 NB = 8;
 
-template <bool SM, bool UF>
+
+template <bool SM, bool UF, u32 NB = dtr::NB>
 __device__ __forceinline__ void nbr_components_phased(const Sim<SM> &g, const uint4 &sr, const uint4 &ar,
                                                       u64 &sum, u32 &L, u64 &bytes) {
   const u32 deg = ar.y + ar.w;
@@ -603,7 +673,8 @@ __device__ __forceinline__ u32 stale_key(u32 c, u32 m, u32 L, u32 clock1) {
 // bound of its score) pairs.  e = null: no stack (the caller re-scans instead).
 struct SlowStack {
   uint2 *e;
-  u32 cap;   // pairs; >= 32 * U + 32 where it is used
+  u32 cap;     // pairs; >= 32 * U + 32 where it is used
+  u64 *msum;   // 32 sums of the multi-candidate closure walk (closure_multi)
 };
 
 // Drain a warp's stack down to `keep` entries: first drop every entry whose
@@ -708,10 +779,13 @@ __device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u
       else stale_score((u64)s4.y + sum, s4.x, L, cmd.clock, c.num, c.den);
       cand_take(best, bk, c);
     };
+    // all lanes' degrees <= 4 (the common case on the recurrent logs): half-width phases
+    const bool narrow = __all_sync(FULL, t == NONE || ar.y + ar.w <= 4);
     if (t != NONE && !big) {
       u64 sum;
       u32 L;
-      nbr_components_phased<SM, UF>(g, sr, ar, sum, L, bytes);
+      if (narrow) nbr_components_phased<SM, UF, 4>(g, sr, ar, sum, L, bytes);
+      else nbr_components_phased<SM, UF>(g, sr, ar, sum, L, bytes);
       finish(t, sr, sum, L);
     }
     u32 bm = __ballot_sync(FULL, big);
@@ -907,6 +981,34 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
 #ifdef DTR_PROFILE
     { const u32 m = __ballot_sync(FULL, t != NONE); if (lane == 0) PROF_ADD(17, __popc(m)); }
 #endif
+    if constexpr (!SM) {
+      // two or more stale candidates: one walk over the union of their closures
+      if (g.L.msps_d && st.msum && __popc(__ballot_sync(FULL, t != NONE)) >= 2) {
+        u32 slot = wrank;
+        if (locked) {                          // acquire a free slot (its holder always finishes)
+          if (lane == 0) {
+            u32 k = wrank % g.L.msps_warps;
+            while (atomicCAS(&g.m.w(g.L.msps_lock + k), 0u, 1u) != 0u) k = k + 1 == g.L.msps_warps ? 0 : k + 1;
+            __threadfence();
+            slot = k;
+          }
+          slot = __shfl_sync(FULL, slot, 0);
+        }
+        u64 up = 0, dn = 0;
+        const bool okm = closure_multi(g, t, slot, msps_tail + (threadIdx.x >> 5), st.msum, down, up, dn, bytes);
+        if (locked && lane == 0) { __threadfence(); atomicExch(&g.m.w(g.L.msps_lock + slot), 0u); }
+        if (lane == 0) PROF_ADD(19 + 5, 1);
+        if (okm) {
+          if (t != NONE) {
+            const uint4 sr = g.srec(t);
+            if (use_cc) g.ccache(t) = make_uint2((u32)up + 1u, down ? (u32)dn + 1u : 0u);
+            cand_take(best, bk, make(t, sr, up + dn));
+            bytes += 16;
+          }
+          return;
+        }
+      }
+    }
     uint4 sr = make_uint4(0, 0, 0, 0);
     uint2 cc = make_uint2(0, 0);
     if (t != NONE) { sr = g.srec(t); if (use_cc) cc = g.ccache(t); }
@@ -1023,7 +1125,7 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
 template <bool SM, bool BM, bool WIDE = false, bool CL = true>
 __device__ Cand team_score(const Sim<SM> &g, const Cmd &cmd, u32 rank, u32 size, u32 wrank, u32 wsize,
                            volatile u32 *msps_tail, u64 &bytes, u64 &evals, u32 &bk,
-                           const SlowStack &st = SlowStack{nullptr, 0}, u32 *sbest = nullptr) {
+                           const SlowStack &st = SlowStack{nullptr, 0, nullptr}, u32 *sbest = nullptr) {
   Cand best = cand_none();
   bk = KEY_NONE;
   if (BM && rank == 0) bytes += (cmd.n_ids + 7) / 8;     // the pool bitmap

@@ -32,4 +32,5 @@ print(f"{m} {h} pm={pm} n={v.n} dec={d} remats={int(r['remats'])} st={int(r['sta
       f"  closure cache: hits {buf[16] / max(d, 1):.1f}/dec, lane walks {buf[17] / max(d, 1):.1f}/dec, "
       f"warp BFS {buf[18] / max(d, 1):.2f}/dec, events {buf[19] / max(d, 1):.2f}/dec, "
       f"event-walk nodes {buf[20] / max(d, 1):.1f}/dec, event cycles {buf[21] / max(d, 1):.0f}/dec\n"
-      f"  stacked (slow/stale) {buf[22] / max(d, 1):.1f}/dec, resolved after pruning {buf[23] / max(d, 1):.1f}/dec", flush=True)
+      f"  stacked (slow/stale) {buf[22] / max(d, 1):.1f}/dec, resolved after pruning {buf[23] / max(d, 1):.1f}/dec, "
+      f"multi-candidate walks {buf[24] / max(d, 1):.2f}/dec", flush=True)
