@@ -57,21 +57,22 @@ from dtr_inputs import LogView, models  # noqa: E402
 
 METRIC = "eviction decisions/sec (pool score+argmin) and sweep runs/sec at 1/2/4/8 B200"
 C5_MODELS = ("resnet32", "densenet100", "unet", "lstm", "treelstm", "transformer")
-C5_HEURS = ("dtr", "dtr_eq", "lru", "size", "msps")
+C5_HEURS = ("dtr", "dtr_eq", "lru", "size")      # the headline; MSPS: --msps (config5_msps)
 C2_HEURS = ("dtr", "dtr_eq", "lru", "size")
 HEUR_IDS = {"dtr": 0, "dtr_eq": 1, "lru": 2, "size": 3, "msps": 4, "local": 5, "random": 6}
-C5_WORKLOAD = ("config5: 6 models {resnet32,densenet100,unet,lstm,treelstm,transformer} x 30 budget ratios x "
-               "{h_DTR,h_DTR_eq,LRU,size,MSPS} = 900 cells, every cell run to its end (no decision cap)")
+C5_WORKLOAD = ("config5 (h_DTR, h_DTR_eq, LRU, size): 6 models {resnet32,densenet100,unet,lstm,treelstm,transformer} "
+               "x 30 budget ratios x 4 heuristics = 720 cells, every cell run to its end (no decision cap); the "
+               "180 MSPS cells of the 900-cell sweep are timed separately (--msps, config5_msps)")
 ORACLE_CAP = 500    # cpu_baseline / reference arm: the first <= ORACLE_CAP decisions of each cell
 
 
-def workload_c5():
-    """config 5: the 900-cell sweep (seed-0 logs), uncapped."""
+def workload_c5(heurs=C5_HEURS):
+    """config 5: the budget x heuristic sweep (seed-0 logs), uncapped."""
     logs = [models.CONFIG_MODELS[m]() for m in C5_MODELS]
     views = [LogView(w) for w in logs]
     cells = []                      # = sweep.make_cells (the reference arm does not import the product)
     for li, v in enumerate(views):
-        for h in C5_HEURS:
+        for h in heurs:
             for pm in models.sweep_permilles(30):
                 cells.append(dict(cell_id=len(cells), log=li, permille=pm, budget=v.budget(pm),
                                   heuristic=HEUR_IDS[h], thrash_kill=16, max_decisions=0))
@@ -275,6 +276,8 @@ def main():
     ap.add_argument("--large-n", type=int, default=1000000)
     ap.add_argument("--large-n2", type=int, default=4000000, help="second large-pool point (0 = skip)")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-2 / config-4 / config-5s extras")
+    ap.add_argument("--msps", action="store_true",
+                    help="also replay the 180 MSPS cells of the config-5 sweep once (config5_msps; minutes)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -435,6 +438,8 @@ def main():
         out["config2_sweep"] = config2(P, torch, dev, flush)
         out["config4"] = config4(P, torch, dev, not args.no_cpu)
         out["config5s"] = config5s(P, torch, dev, not args.no_cpu)
+    if rank == 0 and ws == 1 and args.msps:
+        out["config5_msps"] = config5_msps(P, torch, dev)
     if rank == 0 and ws == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(logs, cells, host_cores())
     if rank == 0:
@@ -507,6 +512,31 @@ def config4(P, torch, dev, with_oracle=True):
             del b
         res[name] = ent
     return res
+
+
+def config5_msps(P, torch, dev):
+    """The 180 MSPS cells of the config-5 sweep (6 models x 30 budget ratios), each
+    run to its end, in one replay (CTA engine, longest first by the static
+    estimate); device time, decisions, and the slowest cell per model."""
+    from paper_2006_09616_b200 import sweep
+    logs, views, cells = workload_c5(("msps",))
+    rs = sweep.RankSweep(logs, views, cells, device=dev.index)
+    s = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    rs.run(s)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rows = np.concatenate([b.result_rows() for b in rs.batches])
+    by = {}
+    for r in rows:
+        m = C5_MODELS[cells[int(r["cell_id"])]["log"]]
+        by[m] = max(by.get(m, 0.0), int(r["wall_ns"]) / 1e6)
+    dec = int(rows["decisions"].sum())
+    return {"workload": "config5 MSPS: 6 models x 30 budget ratios = 180 cells, every cell run to its end",
+            "ms": ms, "decisions": dec, "decisions_per_s": dec / ms * 1e3, "runs_per_s": len(cells) / ms * 1e3,
+            "slowest_cell_ms_by_model": by}
 
 
 def config5s(P, torch, dev, with_oracle=True, D=10000):

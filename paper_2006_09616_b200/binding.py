@@ -245,10 +245,12 @@ class DeviceBatch:
         return sum(1 for i in range(len(cls)) if i == 0 or cls[i] != cls[i - 1])
 
     def run(self, stream=None):
-        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
-        replay_batch(self.words.data_ptr(), self.cells.data_ptr(), self.h_dims, self.n_cells, self.engine,
-                     self.ws.data_ptr(), self.ws_bytes, self.rows.data_ptr(),
-                     self.trace.data_ptr() if self.trace is not None else None, s.cuda_stream)
+        # every dtr_* entry point works on the current device: make it the one that owns the buffers
+        with self.torch.cuda.device(self.device):
+            s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+            replay_batch(self.words.data_ptr(), self.cells.data_ptr(), self.h_dims, self.n_cells, self.engine,
+                         self.ws.data_ptr(), self.ws_bytes, self.rows.data_ptr(),
+                         self.trace.data_ptr() if self.trace is not None else None, s.cuda_stream)
 
     def pool_argmin(self, cell=0, stream=None):
         """dtr_pool_argmin over the grid-engine workspace (call after run()).
@@ -315,11 +317,13 @@ class AdversaryBatch:
         self.trace = torch.zeros(max(toff, 1) * TRACE_DTYPE.itemsize, dtype=torch.uint8, device=dev) if toff else None
 
     def run(self, stream=None):
-        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
-        _check(lib.dtr_adversary_batch(self.d_runs.data_ptr(), _np_ptr(self.h_runs), self.n_runs, self.ws.data_ptr(),
-                                       self.ws_bytes, self.rows.data_ptr(), self.parents.data_ptr(),
-                                       self.trace.data_ptr() if self.trace is not None else None, s.cuda_stream),
-               "dtr_adversary_batch")
+        with self.torch.cuda.device(self.device):
+            s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+            _check(lib.dtr_adversary_batch(self.d_runs.data_ptr(), _np_ptr(self.h_runs), self.n_runs,
+                                           self.ws.data_ptr(), self.ws_bytes, self.rows.data_ptr(),
+                                           self.parents.data_ptr(),
+                                           self.trace.data_ptr() if self.trace is not None else None, s.cuda_stream),
+                   "dtr_adversary_batch")
 
     def result_rows(self):
         return self.rows.cpu().numpy().view(RESULT_DTYPE).copy()

@@ -184,13 +184,20 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
     while (i < n_cells) {
       u64 need;
       const int c = cls_of(i, &need);
-      u64 smem = c == 2 ? CTA_WQ_BYTES : need;   // global state: only the per-warp slow stacks
+      // global state: the per-warp slow stacks (+ the walk mirror of closure cells, if it fits)
+      auto g_smem_of = [&](u32 k) -> u64 {
+        const u32 n = h_dims[3 * k], E = h_dims[3 * k + 1], h = h_dims[3 * k + 2];
+        const u64 m = mirror_ok(n, E, h) ? (u64)CTA_WQ_BYTES + mirror_bytes(n, E) : (u64)CTA_WQ_BYTES;
+        return m <= CTA_SMEM_MAX ? m : (u64)CTA_WQ_BYTES;
+      };
+      u64 smem = c == 2 ? g_smem_of(i) : need;
       u32 j = i + 1;
       bool cl = uses_closure(h_dims[3 * i + 2]);
       for (; j < n_cells; j++) {
         u64 nd;
         if (cls_of(j, &nd) != c) break;
         if (c != 2 && nd > smem) smem = nd;
+        if (c == 2) smem = std::max<u64>(smem, g_smem_of(j));
         cl = cl || uses_closure(h_dims[3 * j + 2]);
       }
       smem = (smem + 15) & ~15ull;
@@ -204,8 +211,13 @@ int dtr_replay_batch(const uint32_t *d_words, const dtr_cell *d_cells, const uin
       }
       if (ds->debug) fprintf(stderr, "dtr: cta launch cells [%u,%u) class %d smem %llu\n", i, j, c, smem);
       // the K5 closure pass is compiled only into the _cl instantiation
-      if (cl) CK(launch_cta_cl(j - i, (u32)smem, ls, d_words, d_cells, i, ws, ws_bytes, d_rows, d_trace));
-      else CK(launch_cta_nocl(j - i, (u32)smem, ls, d_words, d_cells, i, ws, ws_bytes, d_rows, d_trace));
+      if (c == 2) {           // state in global memory: the wide instantiation
+        if (cl) CK(launch_cta_g_cl(j - i, (u32)smem, ls, d_words, d_cells, i, ws, ws_bytes, d_rows, d_trace));
+        else CK(launch_cta_g_nocl(j - i, (u32)smem, ls, d_words, d_cells, i, ws, ws_bytes, d_rows, d_trace));
+      } else {
+        if (cl) CK(launch_cta_cl(j - i, (u32)smem, ls, d_words, d_cells, i, ws, ws_bytes, d_rows, d_trace));
+        else CK(launch_cta_nocl(j - i, (u32)smem, ls, d_words, d_cells, i, ws, ws_bytes, d_rows, d_trace));
+      }
       i = j;
     }
     if (!single) {

@@ -116,6 +116,11 @@ struct Lay {
   u32 e_next, e_child;                                 // linked children (per-call)
   u32 ccache, evq;                                     // closure cache {up+1, down+1} per tensor (0 = stale)
                                                        // + the leader's event queue (batch engines only)
+  // walk mirror (global-state CTA cells of closure heuristics, when the launch's
+  // dynamic shared memory has room): parent CSR as u16 + an evicted bitmap in
+  // shared memory, so closure walks chase pointers at shared-memory latency.
+  // Byte offsets into the dynamic shared memory; mirror = 0: none.
+  u32 mirror, mo_off, mo_par, mo_ev;
   u32 words;                                           // total
 };
 
@@ -152,6 +157,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
   L.msps_bm = L.msps_q = L.msps_words = L.msps_warps = L.msps_lock = L.msps_d = 0;
   L.e_next = L.e_child = 0;
   L.ccache = L.evq = 0;
+  L.mirror = L.mo_off = L.mo_par = L.mo_ev = 0;
   if (heur == H_DTR) {
     L.mem_next = take(n1);
     L.mem_prev = take(n1);
@@ -346,6 +352,30 @@ struct Sim {
     } else {
       for (u32 e = crec(t).x; e != NONE; e = m.w(L.e_next + e)) f(m.w(L.e_child + e));
     }
+  }
+
+  // closure-walk accessors: the shared-memory mirror when present, else the state
+  __device__ __forceinline__ bool wev(u32 x) const {          // is_evicted(state(x))
+    if (L.mirror) return (reinterpret_cast<const u32 *>(reinterpret_cast<const char *>(g_smem) + L.mo_ev)[x >> 5] >> (x & 31)) & 1u;
+    return is_evicted(state(x));
+  }
+  __device__ __forceinline__ uint2 wprec(u32 x) const {       // {par_off, npar}
+    if (L.mirror) {
+      const unsigned short *o = reinterpret_cast<const unsigned short *>(reinterpret_cast<const char *>(g_smem) + L.mo_off);
+      const u32 a = o[x], b = o[x + 1];
+      return make_uint2(a, b - a);
+    }
+    return prec(x);
+  }
+  __device__ __forceinline__ u32 wpar(u32 j) const {
+    if (L.mirror) return reinterpret_cast<const unsigned short *>(reinterpret_cast<const char *>(g_smem) + L.mo_par)[j];
+    return par(j);
+  }
+  __device__ __forceinline__ void mirror_bit(u32 x, bool ev) const {   // leader: x's evicted status flipped
+    if (!L.mirror) return;
+    u32 *w = reinterpret_cast<u32 *>(reinterpret_cast<char *>(g_smem) + L.mo_ev) + (x >> 5);
+    if (ev) *w |= 1u << (x & 31);
+    else *w &= ~(1u << (x & 31));
   }
 
   // union-find find without compression (read-only: safe inside the parallel score pass)

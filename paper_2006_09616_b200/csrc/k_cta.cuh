@@ -38,7 +38,7 @@ __device__ __forceinline__ Cmd shfl_cmd(const Cmd &c) {
 // less cold code (measured 3.5 % faster on the bench's critical cells).
 template <bool SM, bool CL>
 __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_result *row, dtr_evict_rec *trace,
-                        CtaShared &sh) {
+                        CtaShared &sh, u32 smem_bytes) {
   const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Sim<SM> g;
   g.m.gbase = gbase;
@@ -46,13 +46,33 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   PROF_T(ti0);
   const u64 t_start = gtimer();
   init_sim(g, logw, tid, blockDim.x, true, sh.scan, CtaSync());
+  if constexpr (!SM) {
+    // closure heuristics: the walk mirror after the stacks, when the launch reserved room for it
+    const u32 n = g.L.n, E = g.L.E;
+    const u32 base = (blockDim.x >> 5) * (CTA_WQ_PAIRS * 8 + 32 * 8);
+    if (mirror_ok(n, E, cell.heuristic) && base + mirror_bytes(n, E) <= smem_bytes) {
+      g.L.mirror = 1;
+      g.L.mo_off = base;
+      g.L.mo_par = base + (u32)(((u64)2 * (n + 1) + 3) & ~3ull);
+      g.L.mo_ev = g.L.mo_par + (u32)(((u64)2 * E + 3) & ~3ull);
+      const u32 *loff = logw + 16 + 2 * n, *lpar = loff + n + 1;
+      unsigned short *o = reinterpret_cast<unsigned short *>(reinterpret_cast<char *>(g_smem) + g.L.mo_off);
+      unsigned short *pp = reinterpret_cast<unsigned short *>(reinterpret_cast<char *>(g_smem) + g.L.mo_par);
+      u32 *ev = reinterpret_cast<u32 *>(reinterpret_cast<char *>(g_smem) + g.L.mo_ev);
+      for (u32 t = tid; t <= n; t += blockDim.x) o[t] = (unsigned short)loff[t];
+      for (u32 j = tid; j < E; j += blockDim.x) pp[j] = (unsigned short)lpar[j];
+      for (u32 w = tid; w <= (n + 31) / 32; w += blockDim.x) ev[w] = 0;
+      __syncthreads();
+    }
+  }
   PROF_T(ti1);
   if (tid == 0) PROF_ADD(6, ti1 - ti0);
   u64 bytes = 0, evals = 0;
   // global-memory state: the dynamic shared memory holds the per-warp slow stacks (score_stream)
+  const u32 nwarps = blockDim.x >> 5;
   const SlowStack wq = SM ? SlowStack{nullptr, 0, nullptr}
                           : SlowStack{reinterpret_cast<uint2 *>(g_smem) + warp * CTA_WQ_PAIRS, CTA_WQ_PAIRS,
-                                      reinterpret_cast<u64 *>(g_smem + 2 * (CTA_THREADS / 32) * CTA_WQ_PAIRS) + 32 * warp};
+                                      reinterpret_cast<u64 *>(g_smem + 2 * nwarps * CTA_WQ_PAIRS) + 32 * warp};
   if (warp == 0) {
     Leader<SM, false> L;
     if (lane == 0) leader_init(L, g, logw, cell, trace);
@@ -118,11 +138,14 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   if (tid == 0) { row->score_bytes = bytes; row->cand_evals = evals; }
 }
 
-template <bool CL>
-__global__ void __launch_bounds__(CTA_THREADS, 1) cta_engine(const u32 *words, const dtr_cell *cells, u32 c0, u32 n_run,
-                                                          char *ws, u64 ws_bytes, dtr_result *rows,
-                                                          dtr_evict_rec *trace, u32 smem_bytes) {
-  __shared__ CtaShared sh;
+// G = false: cells whose state is staged in shared memory (CTA_THREADS);
+// G = true: cells whose state stays in the global workspace (CTA_G_THREADS:
+// twice the warps to hide the L2 latency of the score pass; the leader then
+// compiles under 128 registers, as in the whole-GPU engine)
+template <bool CL, bool G>
+__device__ __forceinline__ void cta_body(const u32 *words, const dtr_cell *cells, u32 c0, u32 n_run, char *ws,
+                                         u64 ws_bytes, dtr_result *rows, dtr_evict_rec *trace, u32 smem_bytes,
+                                         CtaShared &sh) {
   const u32 tid = threadIdx.x;
   if (blockIdx.x >= n_run) return;
   const u32 ci = c0 + blockIdx.x;
@@ -141,7 +164,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) cta_engine(const u32 *words, c
   const u32 *logw = words + cell.log_offset;
   const u64 off = WS_HEADER + part;
   const u64 mine = cell_bytes(logw[2], logw[3], cell.heuristic, DTR_ENGINE_CTA);
-  if (mine == 0 || off + mine > ws_bytes) {
+  const bool fits = cta_smem_need(logw[2], logw[3], cell.heuristic) <= smem_bytes;
+  if (mine == 0 || off + mine > ws_bytes || fits == G) {   // G launches take exactly the cells that do not fit
     if (tid == 0) {
       dtr_result r; memset(&r, 0, sizeof r);
       r.cell_id = cell.cell_id; r.status = ST_CAPACITY;
@@ -149,10 +173,22 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) cta_engine(const u32 *words, c
     }
     return;
   }
-  if (cta_smem_need(logw[2], logw[3], cell.heuristic) <= smem_bytes)
-    run_cta<true, CL>(logw, cell, nullptr, &rows[ci], trace, sh);
-  else
-    run_cta<false, CL>(logw, cell, (u32 *)(ws + off), &rows[ci], trace, sh);
+  if constexpr (G) run_cta<false, CL>(logw, cell, (u32 *)(ws + off), &rows[ci], trace, sh, smem_bytes);
+  else run_cta<true, CL>(logw, cell, nullptr, &rows[ci], trace, sh, smem_bytes);
 }
 
+template <bool CL>
+__global__ void __launch_bounds__(CTA_THREADS, 1) cta_engine(const u32 *words, const dtr_cell *cells, u32 c0, u32 n_run,
+                                                          char *ws, u64 ws_bytes, dtr_result *rows,
+                                                          dtr_evict_rec *trace, u32 smem_bytes) {
+  __shared__ CtaShared sh;
+  cta_body<CL, false>(words, cells, c0, n_run, ws, ws_bytes, rows, trace, smem_bytes, sh);
+}
 
+template <bool CL>
+__global__ void __launch_bounds__(CTA_G_THREADS, 1) cta_engine_g(const u32 *words, const dtr_cell *cells, u32 c0,
+                                                              u32 n_run, char *ws, u64 ws_bytes, dtr_result *rows,
+                                                              dtr_evict_rec *trace, u32 smem_bytes) {
+  __shared__ CtaShared sh;
+  cta_body<CL, true>(words, cells, c0, n_run, ws, ws_bytes, rows, trace, smem_bytes, sh);
+}

@@ -3,12 +3,20 @@
 
 namespace dtr {
 cudaError_t cta_set_attrs_nocl() {
-  return cudaFuncSetAttribute(cta_engine<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTA_SMEM_MAX);
+  cudaError_t e = cudaFuncSetAttribute(cta_engine<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTA_SMEM_MAX);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(cta_engine_g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTA_SMEM_MAX);
 }
 
 cudaError_t launch_cta_nocl(u32 n_blocks, u32 smem, cudaStream_t st, const u32 *words, const dtr_cell *cells, u32 c0,
                         char *ws, u64 ws_bytes, dtr_result *rows, dtr_evict_rec *trace) {
   cta_engine<false><<<n_blocks, CTA_THREADS, smem, st>>>(words, cells, c0, n_blocks, ws, ws_bytes, rows, trace, smem);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cta_g_nocl(u32 n_blocks, u32 smem, cudaStream_t st, const u32 *words, const dtr_cell *cells,
+                              u32 c0, char *ws, u64 ws_bytes, dtr_result *rows, dtr_evict_rec *trace) {
+  cta_engine_g<false><<<n_blocks, CTA_G_THREADS, smem, st>>>(words, cells, c0, n_blocks, ws, ws_bytes, rows, trace, smem);
   return cudaGetLastError();
 }
 

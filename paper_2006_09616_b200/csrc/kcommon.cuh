@@ -41,9 +41,17 @@ using namespace dtr;
 #define WS_PARTIALS 512
 #define WS_PA_DONE 124       /* dtr_pool_argmin: blocks finished (u32; zeroed by the grid engine) */
 #define CTA_SMEM_MAX (225u * 1024u)
-#define CTA_WQ_PAIRS 1024u   /* global-state cells: per-warp stack of deferred candidates (team.cuh SlowStack) */
-#define CTA_WQ_BYTES (CTA_THREADS / 32 * (CTA_WQ_PAIRS * 8 + 32 * 8))   /* stacks + multi-walk sums: the dynamic
-                                                                        shared memory of those launches */
+#define CTA_WQ_PAIRS 384u    /* global-state cells: per-warp stack of deferred candidates (team.cuh SlowStack) */
+#define CTA_WQ_BYTES (CTA_G_THREADS / 32 * (CTA_WQ_PAIRS * 8 + 32 * 8))   /* stacks + multi-walk sums: the
+                                                                          dynamic shared memory of those launches */
+// walk mirror of a global-state closure cell (engine.cuh Lay.mirror): u16 parent
+// offsets and ids + the evicted bitmap, after the stacks in the dynamic smem
+__host__ __device__ inline u64 mirror_bytes(u32 n, u32 E) {
+  return (((u64)2 * (n + 1) + 3) & ~3ull) + (((u64)2 * E + 3) & ~3ull) + 4ull * ((n + 31) / 32 + 1);
+}
+__host__ __device__ inline bool mirror_ok(u32 n, u32 E, u32 heur) {
+  return uses_closure(heur) && n < 65535 && E < 65535;
+}
 #define GRID_WQ_PAIRS 192u   /* whole-GPU teams: per-warp stack (>= 32 * 4 steps + 32) */  /* + ~1 KB static CtaShared <= 227 KB per block */
 
 // ---------------------------------------------------------------------------
@@ -232,11 +240,13 @@ __host__ __device__ inline u64 cta_smem_need(u32 n, u32 E, u32 heur) {
 
 #define PA_THREADS 256
 
+#define CTA_G_THREADS 512   /* K6 for cells whose state stays in global memory (cta_engine_g) */
+
 struct __align__(16) CtaShared {
   Cmd cmd;
   RedSmem red;
   ScanSmem scan;
-  u32 msps_tail[CTA_THREADS / 32];
+  u32 msps_tail[CTA_G_THREADS / 32];
   u32 best;                          // the CTA team's best pass-1 key (score_stream pruning)
 };
 
@@ -283,6 +293,11 @@ cudaError_t launch_cta_cl(u32 n_blocks, u32 smem, cudaStream_t st, const u32 *wo
                           char *ws, u64 ws_bytes, dtr_result *rows, dtr_evict_rec *trace);
 cudaError_t launch_cta_nocl(u32 n_blocks, u32 smem, cudaStream_t st, const u32 *words, const dtr_cell *cells, u32 c0,
                             char *ws, u64 ws_bytes, dtr_result *rows, dtr_evict_rec *trace);
+// the same for cells whose state stays in global memory (CTA_G_THREADS threads, smem = CTA_WQ_BYTES)
+cudaError_t launch_cta_g_cl(u32 n_blocks, u32 smem, cudaStream_t st, const u32 *words, const dtr_cell *cells, u32 c0,
+                            char *ws, u64 ws_bytes, dtr_result *rows, dtr_evict_rec *trace);
+cudaError_t launch_cta_g_nocl(u32 n_blocks, u32 smem, cudaStream_t st, const u32 *words, const dtr_cell *cells, u32 c0,
+                              char *ws, u64 ws_bytes, dtr_result *rows, dtr_evict_rec *trace);
 // k_grid.cu: K7 and the standalone K3+K4
 cudaError_t grid_occupancy(int *grid_per_sm, int *pa_per_sm);
 cudaError_t launch_grid(int blocks, cudaStream_t st, const u32 *words, const dtr_cell *cells, u32 ci, char *ws,

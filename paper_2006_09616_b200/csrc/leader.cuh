@@ -140,6 +140,7 @@ struct Leader {
       pool_remove(t);
     } else if (is_evicted(st)) {                     // leaves its evicted component
       ev_push(t);
+      g.mirror_bit(t, false);
       nev_add(t, ar, NONE);
       if (s.heuristic == H_DTR) remat_exact(t, ar, st & COMP_MASK);
       else if (uses_uf(s.heuristic)) remat_uf(t, sr.y);
@@ -512,6 +513,7 @@ struct Leader {
     const uint4 sr = g.srec(t);
     const uint4 ar = g.arec(t);
     ev_push(t);
+    g.mirror_bit(t, true);
     g.state(t) = O_BIT;
     s.M -= sr.x;
     pool_remove(t);
@@ -573,6 +575,7 @@ struct Leader {
     if (st & O_BIT) {
       s.remats++;
       ev_push(t);
+      g.mirror_bit(t, false);
       nev_add(t, ar, NONE);
       if (s.heuristic == H_DTR) remat_exact(t, ar, st & COMP_MASK);
       else if (uses_uf(s.heuristic)) remat_uf(t, sr.y);

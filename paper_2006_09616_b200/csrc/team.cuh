@@ -86,7 +86,7 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &ar, u32 wslot, volati
   u64 sum = 0;
   auto visit = [&](u32 p) {
     bytes += 8;   // parent id + its state word
-    if (!is_evicted(g.state(p))) return;
+    if (!g.wev(p)) return;
     u32 bit = 1u << (p & 31);
     u32 old = atomicOr(&g.m.w(bm + (p >> 5)), bit);
     if (old & bit) return;
@@ -95,15 +95,15 @@ __device__ u64 msps_closure(const Sim<SM> &g, const uint4 &ar, u32 wslot, volati
     u32 pos = atomicAdd((u32 *)tail, 1u);
     g.m.w(q + pos) = p;
   };
-  for (u32 j = lane; j < ar.y; j += 32) visit(g.par(ar.x + j));
+  for (u32 j = lane; j < ar.y; j += 32) visit(g.wpar(ar.x + j));
   __syncwarp();
   u32 head = 0, tl = *tail;
   __syncwarp();
   while (head < tl) {
     for (u32 i = head + lane; i < tl; i += 32) {
       u32 x = g.m.w(q + i);
-      const uint2 px = g.prec(x);
-      for (u32 j = 0; j < px.y; j++) visit(g.par(px.x + j));
+      const uint2 px = g.wprec(x);
+      for (u32 j = 0; j < px.y; j++) visit(g.wpar(px.x + j));
     }
     __syncwarp();
     head = tl;
@@ -167,7 +167,7 @@ __device__ void closure_events(const Sim<SM> &g, const Cmd &cmd, u32 slot, volat
   PROF_T(ce0);
   // f = 0: ancestor caches (.x) of the tensors below; f = 1: descendant caches (.y) above
   auto visit = [&](u32 y, u32 f) {
-    if (!is_evicted(g.state(y))) { g.m.w(g.L.ccache + 2 * y + f) = 0; return; }
+    if (!g.wev(y)) { g.m.w(g.L.ccache + 2 * y + f) = 0; return; }
     const u32 bit = 1u << (y & 31);
     if (atomicOr(&g.m.w(bm + (y >> 5)), bit) & bit) return;
     g.m.w(q + atomicAdd((u32 *)tail, 1u)) = y;
@@ -177,8 +177,8 @@ __device__ void closure_events(const Sim<SM> &g, const Cmd &cmd, u32 slot, volat
       const uint2 cr = g.crec(y);
       for (u32 j = 0; j < cr.y; j++) visit(g.m.w(g.L.ch + cr.x + j), 0);
     } else {
-      const uint2 pr = g.prec(y);
-      for (u32 j = 0; j < pr.y; j++) visit(g.par(pr.x + j), 1);
+      const uint2 pr = g.wprec(y);
+      for (u32 j = 0; j < pr.y; j++) visit(g.wpar(pr.x + j), 1);
     }
   };
   u32 nodes = 0;
@@ -233,7 +233,7 @@ __device__ bool closure_multi(const Sim<SM> &g, u32 t, u32 slot, volatile u32 *t
     __syncwarp();
     auto visit = [&](u32 y, u32 m) {
       bytes += 8;                                  // neighbour id + its state word
-      if (!is_evicted(g.state(y))) return;
+      if (!g.wev(y)) return;
       const u32 old = atomicOr(&g.m.w(D + y), m);
       const u32 nb = m & ~old;
       if (!nb) return;
@@ -245,8 +245,8 @@ __device__ bool closure_multi(const Sim<SM> &g, u32 t, u32 slot, volatile u32 *t
     };
     auto expand = [&](u32 x, u32 m) {
       if (!dn_dir) {
-        const uint2 pr = g.prec(x);
-        for (u32 j = 0; j < pr.y; j++) visit(g.par(pr.x + j), m);
+        const uint2 pr = g.wprec(x);
+        for (u32 j = 0; j < pr.y; j++) visit(g.wpar(pr.x + j), m);
       } else {
         const uint2 cr = g.crec(x);
         bytes += 8;
@@ -334,9 +334,9 @@ __device__ __forceinline__ bool closure_lane(const Sim<SM> &g, u32 t, const uint
   auto expand = [&](u32 x, u32 off, u32 cnt) -> bool {
     if constexpr (!DOWN) {
       for (u32 j = 0; j < cnt; j++) {
-        const u32 p = g.par(off + j);
+        const u32 p = g.wpar(off + j);
         b += 8;
-        if (is_evicted(g.state(p)) && !push(p)) return false;
+        if (g.wev(p) && !push(p)) return false;
       }
     } else {
       b += 8;                                            // children record
@@ -344,30 +344,42 @@ __device__ __forceinline__ bool closure_lane(const Sim<SM> &g, u32 t, const uint
         for (u32 j = 0; j < cnt; j++) {
           const u32 c = g.m.w(g.L.ch + off + j);
           b += 8;
-          if (is_evicted(g.state(c)) && !push(c)) return false;
+          if (g.wev(c) && !push(c)) return false;
         }
       } else {
         for (u32 e = g.crec(x).x; e != NONE; e = g.m.w(g.L.e_next + e)) {
           const u32 c = g.m.w(g.L.e_child + e);
           b += 8;
-          if (is_evicted(g.state(c)) && !push(c)) return false;
+          if (g.wev(c) && !push(c)) return false;
         }
       }
     }
     return true;
   };
   if (!(DOWN ? expand(t, ar.z, ar.w) : expand(t, ar.x, ar.y))) return false;
+  // the members' costs are summed four at a time (their loads in flight together,
+  // off the walk's dependent chain)
+  u32 p0 = NONE, p1 = NONE, p2 = NONE, p3 = NONE, np = 0;
+  auto flush = [&]() {
+    const u32 c0 = p0 != NONE ? g.srec(p0).y : 0u, c1 = p1 != NONE ? g.srec(p1).y : 0u;
+    const u32 c2 = p2 != NONE ? g.srec(p2).y : 0u, c3 = p3 != NONE ? g.srec(p3).y : 0u;
+    s += (u64)c0 + c1 + c2 + c3;
+    p0 = p1 = p2 = p3 = NONE;
+    np = 0;
+  };
   u32 last = NONE;
   while (hn) {
     const u32 x = pop();
     if (x == last) continue;
     last = x;
-    s += g.srec(x).y;
+    p3 = p2; p2 = p1; p1 = p0; p0 = x;
+    if (++np == 4) flush();
     b += 16;
     const uint4 ax = DOWN ? g.arec(x) : make_uint4(0, 0, 0, 0);
-    const uint2 px = DOWN ? make_uint2(ax.z, ax.w) : g.prec(x);
+    const uint2 px = DOWN ? make_uint2(ax.z, ax.w) : g.wprec(x);
     if (!expand(x, px.x, px.y)) return false;
   }
+  flush();
   sum = s;
   bytes += b;
   return true;
@@ -983,7 +995,7 @@ __device__ __forceinline__ void team_closure(const Sim<SM> &g, const Cmd &cmd, u
 #endif
     if constexpr (!SM) {
       // two or more stale candidates: one walk over the union of their closures
-      if (g.L.msps_d && st.msum && __popc(__ballot_sync(FULL, t != NONE)) >= 2) {
+      if (g.L.msps_d && !g.L.mirror && st.msum && __popc(__ballot_sync(FULL, t != NONE)) >= 2) {
         u32 slot = wrank;
         if (locked) {                          // acquire a free slot (its holder always finishes)
           if (lane == 0) {
