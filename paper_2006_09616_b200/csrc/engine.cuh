@@ -121,6 +121,12 @@ struct Lay {
   // shared memory, so closure walks chase pointers at shared-memory latency.
   // Byte offsets into the dynamic shared memory; mirror = 0: none.
   u32 mirror, mo_off, mo_par, mo_ev;
+  // h_DTR_eq (batch engines): per tensor the max union-find-root maxla of its
+  // adjacent evicted components at its last exact score, + 1 (0 = none).  Root
+  // maxla never decreases (reading C-9) and the adjacent roots only merge while
+  // no neighbour flips, so it stays a LOWER bound of that max until the leader
+  // clears it on a neighbour's flip: a tighter pruning bound (score_stream).
+  u32 lcache;
   u32 words;                                           // total
 };
 
@@ -128,8 +134,9 @@ struct Lay {
 // layout does not fit 32-bit word offsets (the caller reports DTR_E_CAPACITY).
 // msps_warps: closure-BFS scratch slots (one per scoring warp on a CTA; on the
 // whole-GPU engine a bounded number of slots that warps lock, grid_closure_slots).
-// multi: closure heuristics get the per-slot mask arrays of the multi-candidate
-// walk (closure_multi; global-state cells and the whole-GPU engine only).
+// multi (global-state cells and the whole-GPU engine): closure heuristics get the
+// per-slot mask arrays of the multi-candidate walk (closure_multi), h_DTR_eq the
+// lcache pruning bound (score_stream).
 __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 linked, u32 msps_warps,
                                             u32 grid = 0, u32 multi = 0) {
   u64 o = 0;
@@ -158,6 +165,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
   L.e_next = L.e_child = 0;
   L.ccache = L.evq = 0;
   L.mirror = L.mo_off = L.mo_par = L.mo_ev = 0;
+  L.lcache = 0;
   if (heur == H_DTR) {
     L.mem_next = take(n1);
     L.mem_prev = take(n1);
@@ -171,6 +179,7 @@ __host__ __device__ inline bool make_layout(Lay &L, u32 n, u32 E, u32 heur, u32 
     L.node_of = take(n1);
     L.uf = take(4 * (u64)L.uf_cap);
     L.uf_size = take(L.uf_cap);
+    if (heur == H_DTR_EQ && !linked && multi) L.lcache = take(n1);
   } else if (uses_closure(heur)) {
     L.msps_warps = msps_warps;
     L.msps_words = (u32)((n1 + 31) / 32);

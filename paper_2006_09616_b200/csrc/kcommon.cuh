@@ -110,6 +110,7 @@ __device__ void init_sim(const Sim<SM> &g, const u32 *logw, u32 rank, u32 size, 
     if (heur == H_DTR) g.m.w(g.L.stamp + t) = 0;
     if (uses_uf(heur)) g.m.w(g.L.node_of + t) = NONE;
     if (g.L.ccache) g.ccache(t) = make_uint2(0, 0);
+    if (g.L.lcache) g.m.w(g.L.lcache + t) = 0;
   }
   for (u32 j = rank; j < E; j += size) g.par(j) = lpar[j];
   for (u32 w = rank; w < g.L.pool_words; w += size) g.pool_word(w) = 0;

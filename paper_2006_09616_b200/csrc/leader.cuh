@@ -166,7 +166,8 @@ struct Leader {
   // resident then), where it is reset anyway for the linked (per-call) lists.
   __device__ __forceinline__ void nev_add(u32 t, const uint4 &ar, u32 d) {
     if (!g.L.track_nev) return;
-    g.for_each_nbr(t, ar, [&](u32 q) { g.nev(q) += d; });
+    if (g.L.lcache) g.for_each_nbr(t, ar, [&](u32 q) { g.nev(q) += d; g.m.w(g.L.lcache + q) = 0; });
+    else g.for_each_nbr(t, ar, [&](u32 q) { g.nev(q) += d; });
   }
 
   // ------------------------------------------------------------- exact components
@@ -469,6 +470,7 @@ struct Leader {
     g.m.w(g.L.node_of + t) = n0;
     g.for_each_nbr(t, ar, [&](u32 q) {
       g.nev(q) += 1;
+      if (g.L.lcache) g.m.w(g.L.lcache + q) = 0;        // q's evicted neighbourhood changed
       if (is_evicted(g.state(q))) uf_union(n0, g.m.w(g.L.node_of + q));
     });
   }

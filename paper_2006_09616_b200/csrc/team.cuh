@@ -469,7 +469,7 @@ constexpr u32 NB = 8;
 
 template <bool SM, bool UF, u32 NB = dtr::NB>
 __device__ __forceinline__ void nbr_components_phased(const Sim<SM> &g, const uint4 &sr, const uint4 &ar,
-                                                      u64 &sum, u32 &L, u64 &bytes) {
+                                                      u64 &sum, u32 &L, u64 &bytes, u32 *Lr = nullptr) {
   const u32 deg = ar.y + ar.w;
   u32 q[NB], lab[NB];
 #pragma unroll
@@ -517,11 +517,12 @@ __device__ __forceinline__ void nbr_components_phased(const Sim<SM> &g, const ui
     }
   }
   u64 s = 0;
-  u32 mx = sr.z;
+  u32 mx = 0;                               // the components' max la (encoded)
 #pragma unroll
   for (u32 j = 0; j < NB; j++) { s += mk64(cc[j], ch[j]); mx = cl[j] > mx ? cl[j] : mx; }
   sum = s;
-  L = mx;
+  if (Lr) *Lr = mx;
+  L = mx > sr.z ? mx : sr.z;
   bytes += 16 + 8ull * deg + 12ull * nd;     // adjacency record, ids + states, components
 }
 
@@ -597,7 +598,7 @@ __device__ __forceinline__ void score_h(const Sim<SM> &g, const Cmd &cmd, u32 t,
 // la with la(t) (sr.z); bytes are counted per lane.
 template <bool SM, bool UF>
 __device__ __forceinline__ void nbr_components_warp(const Sim<SM> &g, u32 t, const uint4 &sr, u64 &sum, u32 &L,
-                                                    u64 &bytes) {
+                                                    u64 &bytes, u32 *Lr = nullptr) {
   const u32 FULL = 0xffffffffu, lane = threadIdx.x & 31;
   const uint4 ar = g.arec(t);
   const u32 deg = ar.y + ar.w;
@@ -645,6 +646,7 @@ __device__ __forceinline__ void nbr_components_warp(const Sim<SM> &g, u32 t, con
     mx = m2 > mx ? m2 : mx;
   }
   sum = s;
+  if (Lr) *Lr = mx;
   L = mx > sr.z ? mx : sr.z;
 }
 
@@ -784,21 +786,22 @@ __device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u
     uint4 sr = make_uint4(0, 0, 0, 0), ar = make_uint4(0, 0, 0, 0);
     if (t != NONE) { sr = g.srec(t); ar = g.arec(t); }
     const bool big = t != NONE && ar.y + ar.w > NB;
-    auto finish = [&](u32 tt, const uint4 &s4, u64 sum, u32 L) {
+    auto finish = [&](u32 tt, const uint4 &s4, u64 sum, u32 L, u32 Lr) {
       Cand c;
       c.id = tt;
       if constexpr (H == H_ABL) abl_finish((u64)s4.y + sum, s4.x, s4.z, cmd, c);
       else stale_score((u64)s4.y + sum, s4.x, L, cmd.clock, c.num, c.den);
+      if (H == H_DTR_EQ && g.L.lcache) g.m.w(g.L.lcache + tt) = Lr + 1u;
       cand_take(best, bk, c);
     };
     // all lanes' degrees <= 4 (the common case on the recurrent logs): half-width phases
     const bool narrow = __all_sync(FULL, t == NONE || ar.y + ar.w <= 4);
     if (t != NONE && !big) {
       u64 sum;
-      u32 L;
-      if (narrow) nbr_components_phased<SM, UF, 4>(g, sr, ar, sum, L, bytes);
-      else nbr_components_phased<SM, UF>(g, sr, ar, sum, L, bytes);
-      finish(t, sr, sum, L);
+      u32 L, Lr;
+      if (narrow) nbr_components_phased<SM, UF, 4>(g, sr, ar, sum, L, bytes, &Lr);
+      else nbr_components_phased<SM, UF>(g, sr, ar, sum, L, bytes, &Lr);
+      finish(t, sr, sum, L, Lr);
     }
     u32 bm = __ballot_sync(FULL, big);
     while (bm) {
@@ -809,9 +812,9 @@ __device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u
       s4.x = __shfl_sync(FULL, sr.x, l); s4.y = __shfl_sync(FULL, sr.y, l);
       s4.z = __shfl_sync(FULL, sr.z, l); s4.w = __shfl_sync(FULL, sr.w, l);
       u64 sum;
-      u32 L;
-      nbr_components_warp<SM, UF>(g, tt, s4, sum, L, bytes);
-      if (lane == l) finish(tt, s4, sum, L);
+      u32 L, Lr;
+      nbr_components_warp<SM, UF>(g, tt, s4, sum, L, bytes, &Lr);
+      if (lane == l) finish(tt, s4, sum, L, Lr);
     }
   };
   u32 nq = 0;                                  // warp-uniform stack depth
@@ -837,11 +840,19 @@ __device__ __forceinline__ void score_stream(const Sim<SM> &g, const Cmd &cmd, u
     }
     if constexpr (NBR) {
       if (nbr) {                               // evicted neighbours: deferred with their bound key
+        u32 lc[U];                             // h_DTR_eq: cached lower bound of the roots' max la
+#pragma unroll
+        for (u32 j = 0; j < U; j++)
+          lc[j] = (H == H_DTR_EQ && g.L.lcache && ((bits[j] >> lane) & 1u) && sr[j].w) ? g.m.w(g.L.lcache + tid[j]) : 0u;
 #pragma unroll
         for (u32 j = 0; j < U; j++) {
           const bool slow = ((bits[j] >> lane) & 1u) && sr[j].w != 0;
           const u32 m = __ballot_sync(FULL, slow);
-          if (slow) st.e[nq + __popc(m & ((1u << lane) - 1))] = make_uint2(tid[j], own_key(sr[j]));
+          if (slow) {
+            uint4 r = sr[j];
+            if (lc[j] && lc[j] - 1u > r.z) r.z = lc[j] - 1u;   // L >= max(la(t), cached roots' max la)
+            st.e[nq + __popc(m & ((1u << lane) - 1))] = make_uint2(tid[j], own_key(r));
+          }
           nq += __popc(m);
         }
       }
