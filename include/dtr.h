@@ -275,7 +275,9 @@ int dtr_compute(dtr_runtime *rt, uint32_t mem, uint32_t compute, const uint32_t 
                 uint32_t n_parents, uint32_t *out_id);
 /* get(t): rho++ ; DTR_E_PRECOND if rho == 0. */
 int dtr_get(dtr_runtime *rt, uint32_t id);
-/* release(t): rho-- ; at 0, banish_V2: last_access := -inf. */
+/* release(t): rho-- ; at 0 the runtime's deallocation policy
+ * (dtr_config.dealloc, reading C-22): banish_V2 by default (last_access := -inf,
+ * P:303-311), V1 banishing, eager eviction or nothing. */
 int dtr_release(dtr_runtime *rt, uint32_t id);
 /* rematerialize(t): DTR_E_PRECOND unless t is evicted. */
 int dtr_rematerialize(dtr_runtime *rt, uint32_t id);

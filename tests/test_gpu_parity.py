@@ -589,3 +589,24 @@ def test_percall_state_residency_vs_oracle(P, oracle_mod):
             want = [3 if f & 8 else 1 if f & 1 else 2 if f & 2 else 0 for f in fl]
             assert rt.state().tolist() == want, (h, k)
         rt.close()
+
+
+def test_pool_argmin_bench_1e6_vs_oracle(P, oracle_mod):
+    """The bench's roofline_large_pool configuration itself (config-5s stress log, n = 1e6,
+    B = 0.98 peak_total, 1000 grid-engine decisions, then dtr_pool_argmin over the ~980 k
+    pool) equals the oracle's 1001st decision ("check the bench's 1e6
+    dtr_pool_argmin answers against the oracle's next decision")."""
+    import torch
+    w = models.random_dag(1000000, seed=0, cost_max=200)
+    v = LogView(w)
+    B = v.peak_total * 98 // 100
+    D = 1000
+    ref, tr = oracle_mod.replay(w, oracle_mod.HEURISTICS["dtr"], B, max_decisions=D + 1, trace_cap=D + 1)
+    b = P.DeviceBatch([w], [dict(log=0, budget=B, heuristic=0, max_decisions=D)], engine=P.ENGINE_GRID)
+    b.run()
+    out = b.pool_argmin().cpu().numpy().astype(np.uint64)
+    torch.cuda.synchronize()
+    row = b.result_rows()[0]
+    assert int(row["decisions"]) == D
+    nxt = tr[D]
+    assert (int(out[0]), int(out[1]), int(out[2])) == (int(nxt["num"]), int(nxt["den"]), int(nxt["id"]))
