@@ -25,16 +25,18 @@ def nvcc():
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
-    """profile=True builds libdtr_prof.so with clock64 phase counters (probes only)."""
-    lib = LIB if not profile else os.path.join(HERE, "libdtr_prof.so")
+def build(force: bool = False, verbose: bool = False, profile: bool = False, bounds: bool = False) -> str:
+    """profile=True builds libdtr_prof.so with clock64 phase counters (probes only);
+    bounds=True builds libdtr_bounds.so, every state access bounds-checked (tools/bounds_check.sh)."""
+    lib = LIB if not (profile or bounds) else os.path.join(HERE, "libdtr_prof.so" if profile else "libdtr_bounds.so")
     stale = not os.path.exists(lib) or any(os.path.getmtime(d) > os.path.getmtime(lib) for d in DEPS)
     if not (force or stale):
         return lib
-    tag = f"{os.getpid()}{'p' if profile else ''}"
+    tag = f"{os.getpid()}{'p' if profile else ''}{'b' if bounds else ''}"
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    extra = (["-Xptxas", "-v"] if verbose else []) + (["-DDTR_PROFILE"] if profile else [])
+    extra = (["-Xptxas", "-v"] if verbose else []) + (["-DDTR_PROFILE"] if profile else []) + \
+        (["-DDTR_BOUNDS"] if bounds else [])
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + f".{tag}.o")
@@ -53,4 +55,4 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
 
 if __name__ == "__main__":
     import sys
-    print(build(force=True, verbose="-v" in sys.argv, profile="--profile" in sys.argv))
+    print(build(force=True, verbose="-v" in sys.argv, profile="--profile" in sys.argv, bounds="--bounds" in sys.argv))

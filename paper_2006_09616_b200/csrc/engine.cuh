@@ -215,20 +215,40 @@ __host__ __device__ inline u32 grid_closure_slots(u32 n) {
 // ---------------------------------------------------------------------------
 extern __shared__ __align__(16) u32 g_smem[];
 
+// DTR_BOUNDS (tools/bounds_check.sh; the compute-sanitizer is not available on
+// the GPU pool): every access is checked against the simulation's layout size
+// `lim` (words) and traps with the offending offset.
+#ifdef DTR_BOUNDS
+#define DTR_CHECK(o, k)                                                                                    \
+  do {                                                                                                     \
+    if ((u64)(o) + (k) > (u64)lim) {                                                                       \
+      printf("dtr bounds: block %d thread %d offset %u + %u > %u\n", (int)blockIdx.x, (int)threadIdx.x,  \
+             (unsigned)(o), (unsigned)(k), (unsigned)lim);                                                 \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define DTR_CHECK(o, k)
+#endif
+
 template <bool SM>
 struct Mem {
   u32 *gbase;
+  u32 lim = 0xFFFFFFFFu;   // the layout's words (DTR_BOUNDS builds check every access against it)
   // SM = false: gbase is a global-memory pointer; telling the compiler so lets
   // it emit LDG/STG (global) instead of generic LD/ST
   __device__ __forceinline__ u32 &w(u32 off) const {
+    DTR_CHECK(off, 1);
     if constexpr (SM) return g_smem[off];
     else { __builtin_assume(__isGlobal(gbase)); return gbase[off]; }
   }
   __device__ __forceinline__ uint4 &q(u32 off) const {   // off multiple of 4
+    DTR_CHECK(off, 4);
     if constexpr (SM) return reinterpret_cast<uint4 *>(g_smem)[off >> 2];
     else { __builtin_assume(__isGlobal(gbase)); return reinterpret_cast<uint4 *>(gbase)[off >> 2]; }
   }
   __device__ __forceinline__ uint2 &d(u32 off) const {   // off multiple of 2
+    DTR_CHECK(off, 2);
     if constexpr (SM) return reinterpret_cast<uint2 *>(g_smem)[off >> 1];
     else { __builtin_assume(__isGlobal(gbase)); return reinterpret_cast<uint2 *>(gbase)[off >> 1]; }
   }

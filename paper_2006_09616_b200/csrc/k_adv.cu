@@ -57,6 +57,7 @@ __device__ void run_adversary(const dtr_adversary &run, u32 *gbase, dtr_result *
   g.m.gbase = gbase;
   AdvLay A;
   adv_layout(g.L, A, N, B, run.heuristic);
+  g.m.lim = A.words;
   for (u32 w = tid; w < g.L.pool_words; w += blockDim.x) g.pool_word(w) = 0;
   for (u32 t = tid; t <= N; t += blockDim.x) {
     g.srec(t) = make_uint4(0, 0, 0, 0);

@@ -43,6 +43,7 @@ __device__ void run_cta(const u32 *logw, const dtr_cell &cell, u32 *gbase, dtr_r
   Sim<SM> g;
   g.m.gbase = gbase;
   make_layout(g.L, logw[2], logw[3], cell.heuristic, 0, CTA_THREADS / 32, 0, SM ? 0 : 1);
+  g.m.lim = g.L.words;
   PROF_T(ti0);
   const u64 t_start = gtimer();
   init_sim(g, logw, tid, blockDim.x, true, sh.scan, CtaSync());

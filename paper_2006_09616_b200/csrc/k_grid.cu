@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) grid_engine(const u32 *words,
   Sim<false> g;
   g.m.gbase = (u32 *)(ws + WS_HEADER);
   cell_layout(g.L, logw[2], logw[3], cell.heuristic, DTR_ENGINE_GRID);
+  g.m.lim = g.L.words;
   const u32 rank = blockIdx.x * blockDim.x + tid, size = gridDim.x * blockDim.x;
   const u32 wrank = rank >> 5, wsize = size >> 5;
   if (rank == 0) { gstats[0] = 0; gstats[1] = 0; *(u32 *)(ws + WS_PA_DONE) = 0; }
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(PA_THREADS, 4) pool_argmin_kernel(const u32 *l
   Sim<false> g;
   g.m.gbase = (u32 *)(ws + WS_HEADER);
   cell_layout(g.L, logw[2], logw[3], heur, DTR_ENGINE_GRID);
+  g.m.lim = g.L.words;
   const Scalars *sc = (const Scalars *)(ws + WS_SCALARS);
   Cmd cmd;
   cmd.kind = CMD_ARGMIN; cmd.pool_size = sc->pool_size; cmd.clock = sc->clock; cmd.decisions = sc->decisions;

@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(CTA_THREADS) percall_engine(PercallArgs a) {
   Sim<false> g;
   g.m.gbase = a.base;
   g.L = a.L;
+  g.m.lim = g.L.words;
   if (a.init) {
     for (u32 w = tid; w < g.L.pool_words; w += blockDim.x) g.pool_word(w) = 0;
     for (u32 t = tid; t <= g.L.n; t += blockDim.x) {

@@ -483,14 +483,8 @@ __device__ __forceinline__ void nbr_components_phased(const Sim<SM> &g, const ui
     if constexpr (UF) lab[j] = is_evicted(sq) ? g.m.w(g.L.node_of + q[j]) : NONE;
     else lab[j] = is_evicted(sq) ? (sq & COMP_MASK) : NONE;
   }
-  if constexpr (UF) {
-    // union-find roots, every chain in flight together, with path halving: x's
-    // parent becomes its grandparent as the walk passes.  Safe during the parallel
-    // pass: unions happen only in the (idle) leader, a pointer only ever moves to
-    // a strict ancestor, and roots are never written -- concurrent walkers see an
-    // old or a new ancestor, both on the path to the same root (only the sets and
-    // the roots' records are read).
-    u32 up[NB], gp[NB], steps = 0;
+  if constexpr (UF) {                       // union-find roots: every chain advances one step per round
+    u32 up[NB], steps = 0;
 #pragma unroll
     for (u32 j = 0; j < NB; j++) { up[j] = lab[j] != NONE ? g.uf(lab[j]).w : NONE; bytes += lab[j] != NONE ? 4 : 0; }
     for (;;) {
@@ -499,19 +493,8 @@ __device__ __forceinline__ void nbr_components_phased(const Sim<SM> &g, const ui
       for (u32 j = 0; j < NB; j++) more = more || up[j] != lab[j];
       if (!more) break;
 #pragma unroll
-      for (u32 j = 0; j < NB; j++) gp[j] = up[j] != lab[j] ? g.uf(up[j]).w : NONE;
-#pragma unroll
-      for (u32 j = 0; j < NB; j++) {
-        if (up[j] == lab[j]) continue;
-        steps++;
-        if (gp[j] == up[j]) { lab[j] = up[j]; continue; }     // the parent is the root
-        g.uf(lab[j]).w = gp[j];                                // halve
-        lab[j] = gp[j];
-        up[j] = NONE;                                          // reload below
-      }
-#pragma unroll
       for (u32 j = 0; j < NB; j++)
-        if (up[j] == NONE && lab[j] != NONE) up[j] = g.uf(lab[j]).w;
+        if (up[j] != lab[j]) { lab[j] = up[j]; up[j] = g.uf(lab[j]).w; steps++; }
     }
     bytes += 4ull * steps;
   }
