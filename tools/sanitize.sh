@@ -1,4 +1,5 @@
-# compute-sanitizer over every kernel (run on a GPU box: bash tools/sanitize.sh OUTDIR)
+# compute-sanitizer over every kernel (run on a GPU box: bash tools/sanitize.sh OUTDIR).
+# NOTE: compute-sanitizer is closed on the round-2 GPU pool; tools/bounds_check.sh is the substitute.
 O=${1:-gpurun_out/sanitize}
 mkdir -p $O
 for tool in memcheck racecheck synccheck; do
